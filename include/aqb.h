@@ -1,0 +1,158 @@
+/*
+ * aqb.h — C-ABI of the B200-native DiT denoise hot path (libaqb.so).
+ *
+ * The reference (ditplan, arXiv 2505.10584) has no FFI for this path: it is a
+ * pure-Python planner whose only executable piece of the path is the cache
+ * schedule (pkg/src/ditplan/inference.py:48-86).  The denoise step itself is
+ * described only in prose.  Each entry
+ * point below therefore cites the paper op it implements (Table 2 rows,
+ * PAPER.md:246-256, mirrored as BUILTIN_CHUNKS in pkg/src/ditplan/memory.py:92-107)
+ * — that is the interface a maintainer would bind.
+ *
+ * Conventions:
+ *  - plain pointers and sizes only; all buffers (including workspace) are
+ *    allocated by the caller; element strides are in elements;
+ *  - `stream` is a cudaStream_t passed as void*; every call is stream-ordered,
+ *    never synchronises the host and is safe to capture in a CUDA graph;
+ *  - return 0 (AQB_OK) or a negative status; aqb_last_error() describes it
+ *    (thread-local);
+ *  - `run_flag`/`run_if`: when run_flag != NULL the kernel does its work only
+ *    if *run_flag == run_if (device-side cache decision, no host round-trip).
+ *  - bf16 = IEEE bfloat16 stored as uint16; f32 = float.
+ */
+#ifndef AQB_H_
+#define AQB_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AQB_ABI_VERSION 1
+
+#define AQB_OK 0
+#define AQB_EINVAL (-1)
+#define AQB_ECUDA (-2)
+#define AQB_EUNSUPPORTED (-3)
+
+int aqb_abi_version(void);
+const char* aqb_last_error(void);
+int aqb_sm_count(void);
+
+/* ---------------------------------------------------------------------------
+ * "LayerNorm + Scale/Shift" (memory.py:104):
+ *   y[i,:] = bf16( norm(x[i,:]) * (1 + scale) + shift )
+ * norm_kind 0 = LayerNorm (no affine), 1 = RMSNorm (no affine).
+ * x f32 [rows, hidden] (stride ldx); y bf16 (stride ldy); shift/scale f32
+ * [hidden] or NULL.  hidden % 128 == 0, hidden <= 4096.
+ * Optional rel-L1 probe (diffusion cache, north_star): when probe_prev != NULL
+ * (f32 [rows, hidden], dense) the kernel also writes, per row,
+ * probe_partials[row] = sum|m - prev| and probe_partials[rows + row] =
+ * sum|prev| (f32, m = the un-rounded modulated value), then overwrites prev with m.
+ */
+int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* y, int64_t ldy,
+                      int64_t rows, int32_t hidden, float eps, int32_t norm_kind, float* probe_prev,
+                      float* probe_partials, const int32_t* run_flag, int32_t run_if, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Projection GEMMs (AllGather+QKV_Linear, Out_Linear, FFN_Linear1/2, GeLU and
+ * Gate fused as epilogues — PAPER.md:249-252,254,256):
+ *   acc[m,n] = sum_k A[m,k] * W[n,k]       (A, W bf16, K contiguous; tcgen05)
+ * epilogue:
+ *   AQB_EPI_BF16       out bf16 = acc + bias
+ *   AQB_EPI_GELU_BF16  out bf16 = gelu_tanh(acc + bias)
+ *   AQB_EPI_GATE_RES   out f32 (in/out residual) += gate[n] * (acc + bias)
+ *   AQB_EPI_F32        out f32 = acc + bias
+ *   AQB_EPI_EULER      out f32 (latent, in/out) += (*alpha) * (acc + bias);
+ *                      aux bf16 (stride ld_aux) = bf16(new out)   [flow-matching Euler step]
+ * bias/gate f32 [n] or NULL; alpha: device f32 scalar (EULER only).
+ * Requirements: k % 8 == 0, n % 16 == 0, 16-byte aligned rows.
+ */
+#define AQB_EPI_BF16 0
+#define AQB_EPI_GELU_BF16 1
+#define AQB_EPI_GATE_RES 2
+#define AQB_EPI_F32 3
+#define AQB_EPI_EULER 4
+int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t ldw, void* out, int64_t ldo, int64_t m,
+                  int64_t n, int64_t k, const float* bias, const float* gate, int32_t epilogue, const float* alpha,
+                  void* aux, int64_t ld_aux, const int32_t* run_flag, int32_t run_if, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * "Fused QKNorm" (memory.py:103) + 3D RoPE
+ * + Ulysses pack.  src bf16 [rows, 3, heads, D] (row stride ld_src).  For each
+ * row r and head h in [head_begin, head_begin + head_count):
+ *   q = rms(q) * q_w, k = rms(k) * k_w; if (rope_row0 + r) < rope_rows:
+ *   rotate interleaved pairs of q and k by rope_cos/sin[rope_row0 + r, :]
+ *   (f32 [rope_rows, D/2]); v copied.
+ * dst element (r, which, h, d) lives at
+ *   dst + (j / hpg) * dst_group_stride + r * dst_row_stride + which * dst_which_stride
+ *       + (j % hpg) * D + d,   j = h - head_begin, hpg = heads per group.
+ * In place (dst == src, natural strides) is allowed.  D in {32, 64, 128, 256}.
+ */
+int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t heads, int32_t head_begin,
+                     int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
+                     const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows, void* dst,
+                     int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride, int32_t hpg,
+                     const int32_t* run_flag, int32_t run_if, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * "Flash Attention" (memory.py:97): non-causal softmax(QK^T*scale)V
+ * per head, tcgen05/TMEM, TMA-fed.  Rows of head h of Q start at
+ * q + h*q_head_stride with row stride ldq (likewise K, V, O).  bf16 in/out;
+ * f32 softmax statistics.  head_dim in {32, 64, 128}.  seq_kv >= 1.
+ */
+int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const void* k, int64_t ldk,
+                      int64_t k_head_stride, const void* v, int64_t ldv, int64_t v_head_stride, void* o,
+                      int64_t ldo, int64_t o_head_stride, int64_t seq_q, int64_t seq_kv, int32_t heads,
+                      int32_t head_dim, float softmax_scale, const int32_t* run_flag, int32_t run_if, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * AdaLN / timestep GEMV (tiny, per step):  y[n] = act(sum_k W[n,k] * in(x[k]) + b[n]) + add[n]
+ * W bf16 [n, k]; x/b/add/y f32.  in_silu: apply SiLU to x first.  x may be
+ * replaced by sinusoidal timestep features of *t (x == NULL, k even):
+ * feat = [cos(1000 t f_i), sin(1000 t f_i)], f_i = 10000^(-i/(k/2)).
+ */
+int aqb_gemv(const void* w, const float* x, const float* t, const float* b, const float* add, float* y, int64_t n,
+             int64_t k, int32_t in_silu, void* stream);
+
+/* out[i] = a[i % period] + b[i]  (f32) — per-block modulation tables. */
+int aqb_add_bcast(float* out, const float* a, int64_t period, const float* b, int64_t n, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Diffusion cache (north_star).
+ * aqb_rel_l1_reduce: sums[0] = sum partials[0:rows], sums[1] = sum partials[rows:2rows]
+ *   (single CTA, fixed order — deterministic).
+ * aqb_cache_decide: state (int32[4]: step, flag_full, _, _; f32 view at state+2: acc)
+ *   advances one step and decides full/cached with the RelL1 rule
+ *   (schedule.RelL1Policy.decide); writes flags_out[step] and rel_out[step].
+ * aqb_cache_offset: mode 0: off = x (save rear input);  mode 1: off = x - off
+ *   (rear output - input);  mode 2: x = x + off (cached step).  f32 [rows, hidden].
+ * aqb_step_scalars: cur[0] = ts[*idx], cur[1] = dts[*idx]; mode 1: (*idx)++.
+ */
+int aqb_rel_l1_reduce(const float* partials, int64_t rows, float* sums, void* stream);
+int aqb_cache_decide(const float* sums, int32_t* state, float threshold, int32_t warmup, int32_t total_steps,
+                     int32_t force_last, int32_t* flags_out, float* rel_out, void* stream);
+int aqb_cache_offset(float* x, int64_t ldx, float* off, int64_t rows, int32_t hidden, int32_t mode,
+                     const int32_t* run_flag, int32_t run_if, void* stream);
+int aqb_step_scalars(const float* ts, const float* dts, int32_t* idx, float* cur, int32_t mode, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Latent layout: lat f32 [C, T*pt, H*ph, W*pw]  <->  tokens [T*H*W, pt*ph*pw*C]
+ * (token-major, features ordered (pt, ph, pw, c)).  patchify writes f32 tokens
+ * and a bf16 copy (tok_bf16 may be NULL); unpatchify reads f32 tokens.
+ */
+int aqb_patchify(const float* lat, float* tok, void* tok_bf16, int32_t C, int32_t T, int32_t H, int32_t W,
+                 int32_t pt, int32_t ph, int32_t pw, void* stream);
+int aqb_unpatchify(const float* tok, float* lat, int32_t C, int32_t T, int32_t H, int32_t W, int32_t pt,
+                   int32_t ph, int32_t pw, void* stream);
+
+/* Ulysses head->sequence repack: src bf16 [P, rows, hpg*D] -> dst [rows, P*hpg*D] (row stride ld_dst). */
+int aqb_heads_to_seq(const void* src, int64_t rows, int32_t P, int32_t width, void* dst, int64_t ld_dst,
+                     const int32_t* run_flag, int32_t run_if, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* AQB_H_ */

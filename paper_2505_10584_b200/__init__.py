@@ -1,0 +1,69 @@
+"""B200-native DiT denoise hot path of Aquarius (arXiv 2505.10584).
+
+Public API (drop-in for the reference's cache-schedule boundary,
+``ditplan/__init__.py:58-67`` + ``inference.py:21-86,282-315``):
+
+* ``plan_cache``, ``CacheSchedule``, ``CACHE_MODES``,
+  ``DEFAULT_CACHED_COST_FRACTION``, ``dit_parallel_latency``,
+  ``composite_speedup``, ``ConfigError``, ``PlanningError``, ``DimensionError``
+* new: ``RelL1Policy``, ``DiTConfig`` + presets, ``SingleDiT`` / ``MMDiT``
+  (model construction), ``denoise`` (sampler loop), ``latent_shape``,
+  ``token_count``.
+
+The model/sampler symbols need CUDA and ``libaqb.so`` (hand-written sm_100a
+kernels); they are imported lazily so the schedule API works anywhere.
+"""
+
+from .config import (
+    MM_DIT_13B,
+    PRESETS,
+    SINGLE_DIT_2B,
+    TINY_MM,
+    TINY_SINGLE,
+    DiTConfig,
+    VaeSpec,
+    VideoSpec,
+    flops_per_step,
+    latent_shape,
+    token_count,
+)
+from .errors import ConfigError, DimensionError, NativeError, PlanningError
+from .schedule import (
+    CACHE_MODES,
+    DEFAULT_CACHED_COST_FRACTION,
+    CacheSchedule,
+    RelL1Policy,
+    composite_speedup,
+    dit_parallel_latency,
+    front_block_count,
+    no_cache,
+    plan_cache,
+)
+
+__version__ = "0.1.0"
+
+_LAZY = {
+    "SingleDiT": ("model", "SingleDiT"),
+    "MMDiT": ("model", "MMDiT"),
+    "build_model": ("model", "build_model"),
+    "denoise": ("sampler", "denoise"),
+    "DenoiseResult": ("sampler", "DenoiseResult"),
+}
+
+
+def __getattr__(name):
+    if name in _LAZY:
+        import importlib
+
+        mod, attr = _LAZY[name]
+        return getattr(importlib.import_module(f".{mod}", __name__), attr)
+    raise AttributeError(name)
+
+
+__all__ = [
+    "CACHE_MODES", "DEFAULT_CACHED_COST_FRACTION", "CacheSchedule", "ConfigError", "DimensionError",
+    "DiTConfig", "MM_DIT_13B", "NativeError", "PRESETS", "PlanningError", "RelL1Policy", "SINGLE_DIT_2B",
+    "TINY_MM", "TINY_SINGLE", "VaeSpec", "VideoSpec", "composite_speedup", "dit_parallel_latency",
+    "flops_per_step", "front_block_count", "latent_shape", "no_cache", "plan_cache", "token_count",
+    "SingleDiT", "MMDiT", "build_model", "denoise", "DenoiseResult",
+]

@@ -1,0 +1,493 @@
+// HBM-bound kernels of the DiT block (sm_100a): AdaLN norm+modulate (with the
+// diffusion-cache rel-L1 probe fused in), QK-RMSNorm + 3D RoPE (+ Ulysses
+// pack), AdaLN/timestep GEMV, cache-offset and device-side cache decision,
+// latent (un)patchify and the Ulysses head->sequence repack.
+//
+// Design rules (blackwell guide G2/G7/G13): thread->contiguous element,
+// 16-byte vector loads/stores, warp-shuffle reductions, one warp per row
+// so the whole row lives in registers (single HBM read), fp32 statistics.
+#include <cmath>
+
+#include "host.cuh"
+#include "ptx.cuh"
+
+namespace aqb {
+
+AQB_DEV float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+AQB_DEV float4 ld_stream(const float4* p) {
+  float4 r;
+  asm volatile("ld.global.nc.L1::no_allocate.v4.f32 {%0,%1,%2,%3}, [%4];"
+               : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w)
+               : "l"(p));
+  return r;
+}
+
+// ------------------------------------------------------------ norm+modulate
+// One warp per row; NV float4 per lane (hidden = 128 * NV).
+template <int NV>
+__global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__ x, int64_t ldx,
+                                                       const float* __restrict__ shift,
+                                                       const float* __restrict__ scale, __nv_bfloat16* __restrict__ y,
+                                                       int64_t ldy, int64_t rows, float eps, int kind,
+                                                       float* __restrict__ prev, float* __restrict__ partials,
+                                                       const int32_t* flag, int32_t run_if) {
+  if (!gate_open(flag, run_if)) return;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  constexpr int H = NV * 128;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
+  float4 v[NV];
+#pragma unroll
+  for (int j = 0; j < NV; ++j) v[j] = ld_stream(xr + lane + 32 * j);
+  float mean = 0.f;
+  if (kind == 0) {
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < NV; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    mean = warp_sum(s) * (1.f / H);
+  }
+  float ss = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
+    ss += (a * a + b * b) + (c * c + d * d);
+  }
+  const float rstd = rsqrtf(warp_sum(ss) * (1.f / H) + eps);
+  const float4* sh4 = reinterpret_cast<const float4*>(shift);
+  const float4* sc4 = reinterpret_cast<const float4*>(scale);
+  __nv_bfloat16* yr = y + row * ldy;
+  float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
+  float dsum = 0.f, psum = 0.f;
+#pragma unroll
+  for (int j = 0; j < NV; ++j) {
+    const int c4 = lane + 32 * j;
+    const float4 sc = scale ? __ldg(sc4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 sh = shift ? __ldg(sh4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 o;
+    o.x = (v[j].x - mean) * rstd * (1.f + sc.x) + sh.x;
+    o.y = (v[j].y - mean) * rstd * (1.f + sc.y) + sh.y;
+    o.z = (v[j].z - mean) * rstd * (1.f + sc.z) + sh.z;
+    o.w = (v[j].w - mean) * rstd * (1.f + sc.w) + sh.w;
+    *reinterpret_cast<uint2*>(yr + 4 * c4) = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
+    if (pr) {
+      const float4 p = pr[c4];
+      dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
+      psum += (fabsf(p.x) + fabsf(p.y)) + (fabsf(p.z) + fabsf(p.w));
+      pr[c4] = o;
+    }
+  }
+  if (pr) {
+    dsum = warp_sum(dsum);
+    psum = warp_sum(psum);
+    if (lane == 0) {
+      partials[row] = dsum;
+      partials[rows + row] = psum;
+    }
+  }
+}
+
+// ------------------------------------------------------- QK-norm + 3D RoPE
+// One warp per (row, head); lane handles pairs lane, lane+32, ... (D/2 pairs).
+template <int D>
+__global__ void __launch_bounds__(256) qk_norm_rope_kernel(
+    const __nv_bfloat16* __restrict__ src, int64_t ld_src, int64_t rows, int heads, int head_begin, int head_count,
+    const float* __restrict__ qw, const float* __restrict__ kw, float eps, const float* __restrict__ rcos,
+    const float* __restrict__ rsin, int64_t rope_row0, int64_t rope_rows, __nv_bfloat16* dst, int64_t g_stride,
+    int64_t r_stride, int64_t w_stride, int hpg, const int32_t* flag, int32_t run_if) {
+  if (!gate_open(flag, run_if)) return;
+  constexpr int NP = (D / 2 + 31) / 32;  // pairs per lane
+  const int lane = threadIdx.x & 31;
+  const int64_t item = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
+  if (item >= rows * head_count) return;
+  const int64_t r = item / head_count;
+  const int j = static_cast<int>(item - r * head_count);
+  const int h = head_begin + j;
+  const __nv_bfloat16* s = src + r * ld_src;
+  __nv_bfloat16* d = dst + static_cast<int64_t>(j / hpg) * g_stride + r * r_stride + static_cast<int64_t>(j % hpg) * D;
+  const int64_t grow = rope_row0 + r;
+  const bool rope = grow < rope_rows;
+#pragma unroll
+  for (int which = 0; which < 3; ++which) {
+    const __nv_bfloat162* sp =
+        reinterpret_cast<const __nv_bfloat162*>(s + static_cast<int64_t>(which) * heads * D + static_cast<int64_t>(h) * D);
+    float2 e[NP];
+    float ss = 0.f;
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const int p = lane + 32 * i;
+      e[i] = (p < D / 2) ? __bfloat1622float2(sp[p]) : make_float2(0.f, 0.f);
+      ss += e[i].x * e[i].x + e[i].y * e[i].y;
+    }
+    if (which < 2) {
+      const float rstd = rsqrtf(warp_sum(ss) * (1.f / D) + eps);
+      const float* w = which == 0 ? qw : kw;
+#pragma unroll
+      for (int i = 0; i < NP; ++i) {
+        const int p = lane + 32 * i;
+        if (p < D / 2) {
+          const float2 wv = __ldg(reinterpret_cast<const float2*>(w) + p);
+          float a = e[i].x * rstd * wv.x, b = e[i].y * rstd * wv.y;
+          if (rope) {
+            const float c = __ldg(rcos + grow * (D / 2) + p), sn = __ldg(rsin + grow * (D / 2) + p);
+            const float a2 = a * c - b * sn;
+            b = a * sn + b * c;
+            a = a2;
+          }
+          e[i] = make_float2(a, b);
+        }
+      }
+    }
+    __nv_bfloat162* dp = reinterpret_cast<__nv_bfloat162*>(d + static_cast<int64_t>(which) * w_stride);
+#pragma unroll
+    for (int i = 0; i < NP; ++i) {
+      const int p = lane + 32 * i;
+      if (p < D / 2) dp[p] = __floats2bfloat162_rn(e[i].x, e[i].y);
+    }
+  }
+}
+
+// ---------------------------------------------------------------- GEMV
+// y[n] = W[n,:] . in(x) + b[n] + add[n];  x staged in smem (SiLU or timestep features).
+__global__ void __launch_bounds__(256) gemv_kernel(const __nv_bfloat16* __restrict__ W, const float* __restrict__ x,
+                                                   const float* __restrict__ t, const float* __restrict__ b,
+                                                   const float* __restrict__ add, float* __restrict__ y, int64_t n,
+                                                   int k, int in_silu) {
+  extern __shared__ float xs[];
+  const float tv = t ? __ldg(t) : 0.f;
+  const int half = k / 2;
+  for (int i = threadIdx.x; i < k; i += blockDim.x) {
+    float v;
+    if (x) {
+      v = x[i];
+    } else {
+      const int fi = i < half ? i : i - half;
+      const float f = expf(-9.210340371976184f * fi / half);  // ln(10000)
+      const float a = 1000.f * tv * f;
+      v = i < half ? cosf(a) : sinf(a);
+    }
+    if (in_silu) v = v / (1.f + __expf(-v));
+    xs[i] = v;
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int nvec = k / 8;
+  for (int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5); row < n;
+       row += static_cast<int64_t>(gridDim.x) * 8) {
+    const uint4* wr = reinterpret_cast<const uint4*>(W + row * k);
+    float acc = 0.f;
+    for (int v = lane; v < nvec; v += 32) {
+      const uint4 w8 = __ldg(wr + v);
+      const __nv_bfloat162* w2 = reinterpret_cast<const __nv_bfloat162*>(&w8);
+      const float* xv = xs + 8 * v;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 f = __bfloat1622float2(w2[q]);
+        acc += f.x * xv[2 * q] + f.y * xv[2 * q + 1];
+      }
+    }
+    acc = warp_sum(acc);
+    if (lane == 0) y[row] = acc + (b ? b[row] : 0.f) + (add ? add[row] : 0.f);
+  }
+}
+
+__global__ void add_bcast_kernel(float* out, const float* a, int64_t period, const float* b, int64_t n) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    out[i] = a[i % period] + b[i];
+}
+
+// ------------------------------------------------------- diffusion cache
+__global__ void __launch_bounds__(1024) rel_l1_reduce_kernel(const float* partials, int64_t rows, float* sums) {
+  __shared__ float sd[32], sp[32];
+  float d = 0.f, p = 0.f;
+  for (int64_t i = threadIdx.x; i < rows; i += 1024) {
+    d += partials[i];
+    p += partials[rows + i];
+  }
+  d = warp_sum(d);
+  p = warp_sum(p);
+  if ((threadIdx.x & 31) == 0) sd[threadIdx.x >> 5] = d, sp[threadIdx.x >> 5] = p;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    d = warp_sum(sd[threadIdx.x]);
+    p = warp_sum(sp[threadIdx.x]);
+    if (threadIdx.x == 0) sums[0] = d, sums[1] = p;
+  }
+}
+
+__global__ void cache_decide_kernel(const float* sums, int32_t* state, float thr, int warmup, int total,
+                                    int force_last, int32_t* flags_out, float* rel_out) {
+  const int s = state[0] + 1;
+  float* accp = reinterpret_cast<float*>(state + 2);
+  float acc = *accp;
+  const float rel = sums[1] > 0.f ? sums[0] / sums[1] : 0.f;
+  int full;
+  if (s <= (warmup > 1 ? warmup : 1) || (force_last && s == total)) {
+    full = 1;
+    acc = 0.f;
+  } else {
+    acc += rel;
+    if (acc >= thr) {
+      full = 1;
+      acc = 0.f;
+    } else {
+      full = 0;
+    }
+  }
+  state[0] = s;
+  state[1] = full;
+  *accp = acc;
+  if (flags_out && s - 1 < total) flags_out[s - 1] = full;
+  if (rel_out && s - 1 < total) rel_out[s - 1] = rel;
+}
+
+__global__ void cache_offset_kernel(float* x, int64_t ldx, float* off, int64_t rows, int hidden, int mode,
+                                    const int32_t* flag, int32_t run_if) {
+  if (!gate_open(flag, run_if)) return;
+  const int64_t n4 = rows * (hidden / 4);
+  const int h4 = hidden / 4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n4;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / h4, c = i - r * h4;
+    float4* xp = reinterpret_cast<float4*>(x + r * ldx) + c;
+    float4* op = reinterpret_cast<float4*>(off + r * hidden) + c;
+    if (mode == 0) {
+      *op = *xp;
+    } else if (mode == 1) {
+      const float4 a = *xp, b = *op;
+      *op = make_float4(a.x - b.x, a.y - b.y, a.z - b.z, a.w - b.w);
+    } else {
+      const float4 a = *xp, b = *op;
+      *xp = make_float4(a.x + b.x, a.y + b.y, a.z + b.z, a.w + b.w);
+    }
+  }
+}
+
+__global__ void step_scalars_kernel(const float* ts, const float* dts, int32_t* idx, float* cur, int mode) {
+  const int i = *idx;
+  cur[0] = ts[i];
+  cur[1] = dts[i];
+  if (mode == 1) *idx = i + 1;
+}
+
+// ----------------------------------------------------------- latent layout
+__global__ void patchify_kernel(const float* lat, float* tok, __nv_bfloat16* tokb, int C, int T, int H, int W, int pt,
+                                int ph, int pw) {
+  const int F = pt * ph * pw * C;
+  const int64_t n = static_cast<int64_t>(T) * H * W * F;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = i / F;
+    int f = static_cast<int>(i - s * F);
+    const int c = f % C;
+    f /= C;
+    const int iw = f % pw;
+    f /= pw;
+    const int ih = f % ph;
+    const int it = f / ph;
+    const int w = static_cast<int>(s % W), h = static_cast<int>((s / W) % H), t = static_cast<int>(s / (W * H));
+    const float v = lat[((static_cast<int64_t>(c) * T * pt + t * pt + it) * H * ph + h * ph + ih) * W * pw + w * pw + iw];
+    tok[i] = v;
+    if (tokb) tokb[i] = __float2bfloat16(v);
+  }
+}
+
+__global__ void unpatchify_kernel(const float* tok, float* lat, int C, int T, int H, int W, int pt, int ph, int pw) {
+  const int F = pt * ph * pw * C;
+  const int64_t n = static_cast<int64_t>(T) * H * W * F;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t s = i / F;
+    int f = static_cast<int>(i - s * F);
+    const int c = f % C;
+    f /= C;
+    const int iw = f % pw;
+    f /= pw;
+    const int ih = f % ph;
+    const int it = f / ph;
+    const int w = static_cast<int>(s % W), h = static_cast<int>((s / W) % H), t = static_cast<int>(s / (W * H));
+    lat[((static_cast<int64_t>(c) * T * pt + t * pt + it) * H * ph + h * ph + ih) * W * pw + w * pw + iw] = tok[i];
+  }
+}
+
+// src [P, rows, width] -> dst [rows, P*width] (16-byte units)
+__global__ void heads_to_seq_kernel(const uint4* src, int64_t rows, int P, int w16, uint4* dst, int64_t ld16,
+                                    const int32_t* flag, int32_t run_if) {
+  if (!gate_open(flag, run_if)) return;
+  const int64_t n = rows * P * w16;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / (P * w16);
+    const int rem = static_cast<int>(i - r * P * w16);
+    const int p = rem / w16, c = rem - p * w16;
+    dst[r * ld16 + rem] = src[(static_cast<int64_t>(p) * rows + r) * w16 + c];
+  }
+}
+
+static int grid_for(int64_t n, int threads) {
+  int64_t g = (n + threads - 1) / threads;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 32;
+  if (g > cap) g = cap;
+  return static_cast<int>(g < 1 ? 1 : g);
+}
+
+}  // namespace aqb
+
+using namespace aqb;
+
+extern "C" int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* y,
+                                 int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
+                                 float* probe_prev, float* probe_partials, const int32_t* run_flag, int32_t run_if,
+                                 void* stream) {
+  AQB_CHECK_ARG(x && y, "norm_modulate: null pointer");
+  AQB_CHECK_ARG(hidden % 128 == 0 && hidden >= 128 && hidden <= 4096, "norm_modulate: hidden %d unsupported", hidden);
+  AQB_CHECK_ARG(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= hidden && ldy >= hidden, "norm_modulate: bad strides");
+  AQB_CHECK_ARG(!probe_prev || probe_partials, "norm_modulate: probe needs partials");
+  AQB_CHECK_ARG(norm_kind == 0 || norm_kind == 1, "norm_modulate: bad kind");
+  if (rows <= 0) return AQB_OK;
+  const int grid = static_cast<int>((rows + 7) / 8);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
+#define NM_CASE(NV)                                                                                          \
+  case NV:                                                                                                   \
+    norm_mod_kernel<NV><<<grid, 256, 0, s>>>(x, ldx, shift, scale, yb, ldy, rows, eps, norm_kind, probe_prev, \
+                                             probe_partials, run_flag, run_if);                              \
+    break;
+  switch (hidden / 128) {
+    NM_CASE(1) NM_CASE(2) NM_CASE(3) NM_CASE(4) NM_CASE(6) NM_CASE(8) NM_CASE(12) NM_CASE(16) NM_CASE(20)
+    NM_CASE(24) NM_CASE(32)
+    default:
+      return set_error(AQB_EUNSUPPORTED, "norm_modulate: hidden %d not instantiated", hidden);
+  }
+#undef NM_CASE
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t heads, int32_t head_begin,
+                                int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
+                                const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows,
+                                void* dst, int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride,
+                                int32_t hpg, const int32_t* run_flag, int32_t run_if, void* stream) {
+  AQB_CHECK_ARG(src && dst && q_w && k_w, "qk_norm_rope: null pointer");
+  AQB_CHECK_ARG(head_begin >= 0 && head_count >= 1 && head_begin + head_count <= heads, "qk_norm_rope: bad heads");
+  AQB_CHECK_ARG(hpg >= 1 && head_count % hpg == 0, "qk_norm_rope: bad heads-per-group");
+  AQB_CHECK_ARG(rope_rows <= 0 || (rope_cos && rope_sin), "qk_norm_rope: rope tables missing");
+  AQB_CHECK_ARG(ld_src >= 3ll * heads * head_dim, "qk_norm_rope: bad ld_src");
+  if (rows <= 0) return AQB_OK;
+  const int64_t items = rows * head_count;
+  const int grid = static_cast<int>((items + 7) / 8);
+  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
+  auto sp = reinterpret_cast<const __nv_bfloat16*>(src);
+  auto dp = reinterpret_cast<__nv_bfloat16*>(dst);
+#define QK_CASE(D)                                                                                                \
+  case D:                                                                                                         \
+    qk_norm_rope_kernel<D><<<grid, 256, 0, s>>>(sp, ld_src, rows, heads, head_begin, head_count, q_w, k_w, eps,   \
+                                                rope_cos, rope_sin, rope_row0, rope_rows, dp, dst_group_stride,   \
+                                                dst_row_stride, dst_which_stride, hpg, run_flag, run_if);         \
+    break;
+  switch (head_dim) {
+    QK_CASE(32) QK_CASE(64) QK_CASE(128) QK_CASE(256)
+    default:
+      return set_error(AQB_EUNSUPPORTED, "qk_norm_rope: head_dim %d unsupported", head_dim);
+  }
+#undef QK_CASE
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_gemv(const void* w, const float* x, const float* t, const float* b, const float* add, float* y,
+                        int64_t n, int64_t k, int32_t in_silu, void* stream) {
+  AQB_CHECK_ARG(w && y, "gemv: null pointer");
+  AQB_CHECK_ARG(x || t, "gemv: need x or t");
+  AQB_CHECK_ARG(k % 8 == 0 && k >= 8 && k <= 16384, "gemv: k=%lld unsupported", (long long)k);
+  if (n <= 0) return AQB_OK;
+  int64_t g = (n + 7) / 8;
+  const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
+  if (g > cap) g = cap;
+  gemv_kernel<<<static_cast<int>(g), 256, k * sizeof(float), reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const __nv_bfloat16*>(w), x, t, b, add, y, n, static_cast<int>(k), in_silu);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_add_bcast(float* out, const float* a, int64_t period, const float* b, int64_t n, void* stream) {
+  AQB_CHECK_ARG(out && a && b && period >= 1, "add_bcast: bad args");
+  if (n <= 0) return AQB_OK;
+  add_bcast_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out, a, period, b, n);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_rel_l1_reduce(const float* partials, int64_t rows, float* sums, void* stream) {
+  AQB_CHECK_ARG(partials && sums && rows >= 1, "rel_l1_reduce: bad args");
+  rel_l1_reduce_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(partials, rows, sums);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_cache_decide(const float* sums, int32_t* state, float threshold, int32_t warmup,
+                                int32_t total_steps, int32_t force_last, int32_t* flags_out, float* rel_out,
+                                void* stream) {
+  AQB_CHECK_ARG(sums && state && total_steps >= 1, "cache_decide: bad args");
+  cache_decide_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(sums, state, threshold, warmup, total_steps,
+                                                                            force_last, flags_out, rel_out);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_cache_offset(float* x, int64_t ldx, float* off, int64_t rows, int32_t hidden, int32_t mode,
+                                const int32_t* run_flag, int32_t run_if, void* stream) {
+  AQB_CHECK_ARG(x && off && hidden % 4 == 0 && ldx % 4 == 0 && mode >= 0 && mode <= 2, "cache_offset: bad args");
+  if (rows <= 0) return AQB_OK;
+  cache_offset_kernel<<<grid_for(rows * hidden / 4, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      x, ldx, off, rows, hidden, mode, run_flag, run_if);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_step_scalars(const float* ts, const float* dts, int32_t* idx, float* cur, int32_t mode,
+                                void* stream) {
+  AQB_CHECK_ARG(ts && dts && idx && cur, "step_scalars: null pointer");
+  step_scalars_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(ts, dts, idx, cur, mode);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_patchify(const float* lat, float* tok, void* tok_bf16, int32_t C, int32_t T, int32_t H, int32_t W,
+                            int32_t pt, int32_t ph, int32_t pw, void* stream) {
+  AQB_CHECK_ARG(lat && tok && C > 0 && T > 0 && H > 0 && W > 0 && pt > 0 && ph > 0 && pw > 0, "patchify: bad args");
+  const int64_t n = static_cast<int64_t>(C) * T * H * W * pt * ph * pw;
+  patchify_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      lat, tok, reinterpret_cast<__nv_bfloat16*>(tok_bf16), C, T, H, W, pt, ph, pw);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_unpatchify(const float* tok, float* lat, int32_t C, int32_t T, int32_t H, int32_t W, int32_t pt,
+                              int32_t ph, int32_t pw, void* stream) {
+  AQB_CHECK_ARG(lat && tok && C > 0 && T > 0 && H > 0 && W > 0 && pt > 0 && ph > 0 && pw > 0, "unpatchify: bad args");
+  const int64_t n = static_cast<int64_t>(C) * T * H * W * pt * ph * pw;
+  unpatchify_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(tok, lat, C, T, H, W, pt,
+                                                                                           ph, pw);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_heads_to_seq(const void* src, int64_t rows, int32_t P, int32_t width, void* dst, int64_t ld_dst,
+                                const int32_t* run_flag, int32_t run_if, void* stream) {
+  AQB_CHECK_ARG(src && dst && P >= 1 && width % 8 == 0 && ld_dst % 8 == 0 && ld_dst >= int64_t(P) * width,
+                "heads_to_seq: bad args");
+  if (rows <= 0) return AQB_OK;
+  const int w16 = width / 8;
+  heads_to_seq_kernel<<<grid_for(rows * P * w16, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
+      reinterpret_cast<const uint4*>(src), rows, P, w16, reinterpret_cast<uint4*>(dst), ld_dst / 8, run_flag, run_if);
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}

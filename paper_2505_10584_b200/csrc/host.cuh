@@ -1,0 +1,49 @@
+// Host-side helpers shared by the C-ABI entry points: status codes, the
+// thread-local last-error string, TMA descriptor encoding (driver entry point
+// fetched through the runtime, so the library does not link libcuda), and
+// per-device properties.
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <cstdarg>
+#include <mutex>
+
+#include "../../include/aqb.h"
+
+namespace aqb {
+
+int set_error(int code, const char* fmt, ...);
+const char* last_error();
+
+#define AQB_CHECK_ARG(cond, ...)                         \
+  do {                                                   \
+    if (!(cond)) return ::aqb::set_error(AQB_EINVAL, __VA_ARGS__); \
+  } while (0)
+
+#define AQB_CUDA_TRY(expr)                                                                         \
+  do {                                                                                             \
+    cudaError_t _e = (expr);                                                                       \
+    if (_e != cudaSuccess)                                                                         \
+      return ::aqb::set_error(AQB_ECUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, \
+                              __LINE__);                                                           \
+  } while (0)
+
+#define AQB_LAUNCH_CHECK()                                                                      \
+  do {                                                                                          \
+    cudaError_t _e = cudaGetLastError();                                                        \
+    if (_e != cudaSuccess)                                                                      \
+      return ::aqb::set_error(AQB_ECUDA, "launch failed: %s (%s:%d)", cudaGetErrorString(_e), __FILE__, \
+                              __LINE__);                                                        \
+  } while (0)
+
+int sm_count();
+
+// Encode a bf16 tensor map with 128B swizzle.  dims/strides innermost first;
+// strides in bytes for dims 1..rank-1.  Returns 0 or a negative status.
+int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz);
+
+}  // namespace aqb

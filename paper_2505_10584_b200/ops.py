@@ -1,0 +1,147 @@
+"""Torch-facing wrappers over the C-ABI (``include/aqb.h``).
+
+Each wrapper validates device / dtype / layout, then passes raw pointers and
+the *current* CUDA stream to libaqb.so (so calls are stream-ordered and CUDA
+graph capturable).  Nothing here computes on the CPU and there is no
+fallback path: a missing library or a non-CUDA tensor raises.
+"""
+
+from __future__ import annotations
+
+import torch
+
+from . import _native
+from .errors import NativeError
+
+EPI = {"bf16": 0, "gelu": 1, "gate_res": 2, "f32": 3, "euler": 4}
+BF16, F32 = torch.bfloat16, torch.float32
+
+
+def _stream():
+    return torch.cuda.current_stream().cuda_stream
+
+
+def _p(t):
+    return None if t is None else t.data_ptr()
+
+
+def _need(t, dtype, name):
+    if not t.is_cuda:
+        raise NativeError(f"{name}: tensor must be on a CUDA device (no CPU fallback)")
+    if t.dtype != dtype:
+        raise NativeError(f"{name}: expected {dtype}, got {t.dtype}")
+    if t.stride(-1) != 1:
+        raise NativeError(f"{name}: innermost dim must be contiguous")
+
+
+def norm_modulate(x, shift, scale, out, eps=1e-6, kind=0, probe_prev=None, probe_partials=None,
+                  run_flag=None, run_if=1):
+    """out[bf16] = norm(x)·(1+scale)+shift, row-wise over the last dim."""
+    _need(x, F32, "norm_modulate.x")
+    _need(out, BF16, "norm_modulate.out")
+    rows, hidden = x.shape
+    _native.call("aqb_norm_modulate", _p(x), x.stride(0), _p(shift), _p(scale), _p(out), out.stride(0), rows,
+                 hidden, float(eps), int(kind), _p(probe_prev), _p(probe_partials), _p(run_flag), int(run_if),
+                 _stream())
+    return out
+
+
+def gemm(a, w, out, bias=None, gate=None, epilogue="bf16", alpha=None, aux=None, run_flag=None, run_if=1):
+    """out = epilogue(a @ w.T + bias) on tcgen05 (a [M,K] bf16, w [N,K] bf16)."""
+    _need(a, BF16, "gemm.a")
+    _need(w, BF16, "gemm.w")
+    m, k = a.shape
+    n, k2 = w.shape
+    if k2 != k:
+        raise NativeError(f"gemm: K mismatch {k} vs {k2}")
+    e = EPI[epilogue]
+    _need(out, BF16 if e in (0, 1) else F32, "gemm.out")
+    if out.shape[0] != m or out.shape[1] < n:
+        raise NativeError(f"gemm: out shape {tuple(out.shape)} vs ({m},{n})")
+    _native.call("aqb_gemm_bf16", _p(a), a.stride(0), _p(w), w.stride(0), _p(out), out.stride(0), m, n, k,
+                 _p(bias), _p(gate), e, _p(alpha), _p(aux), aux.stride(0) if aux is not None else 0,
+                 _p(run_flag), int(run_if), _stream())
+    return out
+
+
+def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_row0=0, rope_rows=0,
+                 dst=None, head_begin=0, head_count=None, hpg=None, dst_group_stride=0, dst_row_stride=None,
+                 dst_which_stride=None, run_flag=None, run_if=1):
+    """QK-RMSNorm + 3D RoPE over a [rows, 3, heads, D] QKV buffer (optionally repacked into dst)."""
+    _need(src, BF16, "qk_norm_rope.src")
+    rows = src.shape[0]
+    head_count = heads if head_count is None else head_count
+    hpg = head_count if hpg is None else hpg
+    if dst is None:
+        dst = src
+    if dst_row_stride is None:
+        dst_row_stride = dst.stride(0)
+    if dst_which_stride is None:
+        dst_which_stride = heads * head_dim
+    _native.call("aqb_qk_norm_rope", _p(src), src.stride(0), rows, heads, head_begin, head_count, head_dim,
+                 _p(q_w), _p(k_w), float(eps), _p(cos), _p(sin), int(rope_row0), int(rope_rows), _p(dst),
+                 int(dst_group_stride), int(dst_row_stride), int(dst_which_stride), int(hpg), _p(run_flag),
+                 int(run_if), _stream())
+    return dst
+
+
+def attention(q, k, v, o, heads, head_dim, q_head_stride=None, k_head_stride=None, v_head_stride=None,
+              o_head_stride=None, scale=None, run_flag=None, run_if=1):
+    """Non-causal flash attention; q/k/v/o are 2-D row views [seq, ld] (head h at column h*head_stride)."""
+    for t, nm in ((q, "q"), (k, "k"), (v, "v"), (o, "o")):
+        _need(t, BF16, f"attention.{nm}")
+    hs = lambda x: head_dim if x is None else x  # noqa: E731
+    scale = head_dim ** -0.5 if scale is None else scale
+    _native.call("aqb_attention_fwd", _p(q), q.stride(0), hs(q_head_stride), _p(k), k.stride(0), hs(k_head_stride),
+                 _p(v), v.stride(0), hs(v_head_stride), _p(o), o.stride(0), hs(o_head_stride), q.shape[0],
+                 k.shape[0], heads, head_dim, float(scale), _p(run_flag), int(run_if), _stream())
+    return o
+
+
+def gemv(w, x, out, bias=None, add=None, in_silu=False, t=None):
+    """out[f32] = w @ in(x) + bias + add  (x f32, or timestep features of device scalar t)."""
+    _need(w, BF16, "gemv.w")
+    n, k = w.shape
+    _native.call("aqb_gemv", _p(w), _p(x), _p(t), _p(bias), _p(add), _p(out), n, k, int(bool(in_silu)), _stream())
+    return out
+
+
+def add_bcast(out, a, b):
+    _native.call("aqb_add_bcast", _p(out), _p(a), a.numel(), _p(b), b.numel(), _stream())
+    return out
+
+
+def rel_l1_reduce(partials, rows, sums):
+    _native.call("aqb_rel_l1_reduce", _p(partials), rows, _p(sums), _stream())
+
+
+def cache_decide(sums, state, threshold, warmup, total_steps, force_last, flags_out, rel_out):
+    _native.call("aqb_cache_decide", _p(sums), _p(state), float(threshold), int(warmup), int(total_steps),
+                 int(bool(force_last)), _p(flags_out), _p(rel_out), _stream())
+
+
+def cache_offset(x, off, mode, run_flag=None, run_if=1):
+    rows, hidden = off.shape
+    _native.call("aqb_cache_offset", _p(x), x.stride(0), _p(off), rows, hidden, int(mode), _p(run_flag),
+                 int(run_if), _stream())
+
+
+def step_scalars(ts, dts, idx, cur, advance=False):
+    _native.call("aqb_step_scalars", _p(ts), _p(dts), _p(idx), _p(cur), int(bool(advance)), _stream())
+
+
+def patchify(lat, tok, tok_bf16, grid, patch):
+    C = lat.shape[0]
+    _native.call("aqb_patchify", _p(lat), _p(tok), _p(tok_bf16), C, grid[0], grid[1], grid[2], patch[0], patch[1],
+                 patch[2], _stream())
+
+
+def unpatchify(tok, lat, grid, patch):
+    C = lat.shape[0]
+    _native.call("aqb_unpatchify", _p(tok), _p(lat), C, grid[0], grid[1], grid[2], patch[0], patch[1], patch[2],
+                 _stream())
+
+
+def heads_to_seq(src, rows, P, width, dst, run_flag=None, run_if=1):
+    _native.call("aqb_heads_to_seq", _p(src), rows, P, width, _p(dst), dst.stride(0), _p(run_flag), int(run_if),
+                 _stream())

@@ -1,0 +1,232 @@
+"""Per-kernel numerics on the B200, through the C-ABI (libaqb.so).
+
+Each CUDA kernel is compared with a plain fp32 PyTorch statement of the same
+op (the oracle's functions where one exists).  Tolerances are written next to
+each assert; bf16 outputs are checked by relative L2 error.
+"""
+
+import math
+
+import pytest
+import torch
+
+from oracle import dit_oracle as ref
+from paper_2505_10584_b200 import ops
+
+pytestmark = pytest.mark.gpu
+dev = "cuda"
+
+
+def rel_l2(a, b):
+    a, b = a.double().cpu(), b.double().cpu()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+@pytest.mark.parametrize("m,n,k", [(128, 256, 64), (7800, 2048, 2048), (300, 384, 200), (33, 32, 32),
+                                   (1000, 6144, 2048), (257, 128, 4096)])
+def test_gemm_bf16_matches_fp32(m, n, k):
+    g = torch.Generator(device=dev).manual_seed(m + n + k)
+    a = torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(n, device=dev, generator=g)
+    out = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+    ops.gemm(a, w, out, bias=bias)
+    exp = a.float() @ w.float().t() + bias
+    assert rel_l2(out, exp) < 8e-3  # bf16 output rounding (~2^-9) dominates
+
+
+@pytest.mark.parametrize("epi", ["gelu", "gate_res", "f32", "euler"])
+def test_gemm_epilogues(epi):
+    m, n, k = 777, 512, 384
+    g = torch.Generator(device=dev).manual_seed(7)
+    a = torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(n, device=dev, generator=g)
+    acc = a.float() @ w.float().t() + bias
+    if epi == "gelu":
+        out = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+        ops.gemm(a, w, out, bias=bias, epilogue="gelu")
+        assert rel_l2(out, torch.nn.functional.gelu(acc, approximate="tanh")) < 8e-3
+    elif epi == "gate_res":
+        res = torch.randn(m, n, device=dev, generator=g)
+        gate = torch.randn(n, device=dev, generator=g)
+        exp = res + gate * acc
+        ops.gemm(a, w, res, bias=bias, gate=gate, epilogue="gate_res")
+        assert rel_l2(res, exp) < 1e-5  # fp32 epilogue, fp32 accumulation
+    elif epi == "f32":
+        out = torch.empty(m, n, device=dev)
+        ops.gemm(a, w, out, bias=bias, epilogue="f32")
+        assert rel_l2(out, acc) < 1e-5
+    else:
+        x = torch.randn(m, n, device=dev, generator=g)
+        aux = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+        alpha = torch.tensor([0.125], device=dev)
+        exp = x + 0.125 * acc
+        ops.gemm(a, w, x, bias=bias, epilogue="euler", alpha=alpha, aux=aux)
+        assert rel_l2(x, exp) < 1e-5
+        assert rel_l2(aux, exp) < 8e-3
+
+
+def test_gemm_run_flag_skips():
+    a = torch.ones(128, 64, device=dev, dtype=torch.bfloat16)
+    w = torch.ones(64, 64, device=dev, dtype=torch.bfloat16)
+    out = torch.zeros(128, 64, device=dev)
+    flag = torch.tensor([0], device=dev, dtype=torch.int32)
+    ops.gemm(a, w, out, epilogue="f32", run_flag=flag, run_if=1)
+    assert float(out.abs().sum()) == 0.0
+    ops.gemm(a, w, out, epilogue="f32", run_flag=flag, run_if=0)
+    assert torch.allclose(out, torch.full_like(out, 64.0))
+
+
+def _attn_ref(q, k, v):
+    # q [Sq, A, D] fp32 on CPU
+    return ref.attention(q.float().cpu(), k.float().cpu(), v.float().cpu())
+
+
+@pytest.mark.parametrize("sq,skv,heads,d", [(256, 256, 2, 128), (300, 300, 3, 128), (7800 // 8, 7800 // 8, 2, 128),
+                                           (129, 16, 4, 128), (512, 4096, 1, 128), (200, 200, 4, 64),
+                                           (48, 48, 4, 32), (32, 16, 4, 32)])
+def test_attention_packed_qkv(sq, skv, heads, d):
+    """Q/K/V read in place from a [S, 3, A, D] QKV buffer (self-attn layout)."""
+    g = torch.Generator(device=dev).manual_seed(sq * 7 + skv)
+    qkv = torch.randn(max(sq, skv), 3, heads, d, device=dev, generator=g).to(torch.bfloat16)
+    q = qkv[:sq, 0]
+    k = qkv[:skv, 1]
+    v = qkv[:skv, 2]
+    o = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
+    flat = qkv.view(qkv.shape[0], -1)
+    ops.attention(flat[:sq, 0:], flat[:skv, heads * d:], flat[:skv, 2 * heads * d:], o, heads, d)
+    exp = _attn_ref(q, k, v)
+    assert rel_l2(o, exp) < 1e-2  # bf16 P and output rounding
+
+
+def test_attention_large_logits_rescale():
+    """Scores with a large dynamic range exercise the lazy O rescale path."""
+    sq, skv, heads, d = 256, 1024, 2, 128
+    g = torch.Generator(device=dev).manual_seed(11)
+    q = (torch.randn(sq, heads, d, device=dev, generator=g) * 3).to(torch.bfloat16)
+    k = (torch.randn(skv, heads, d, device=dev, generator=g) * 3).to(torch.bfloat16)
+    # make later key tiles dominate so the running max keeps growing
+    k[768:] *= 2
+    v = torch.randn(skv, heads, d, device=dev, generator=g).to(torch.bfloat16)
+    o = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
+    ops.attention(q.view(sq, -1), k.view(skv, -1), v.view(skv, -1), o, heads, d)
+    assert rel_l2(o, _attn_ref(q, k, v)) < 1e-2
+
+
+@pytest.mark.parametrize("hidden,kind", [(128, 0), (2048, 0), (3072, 0), (2048, 1)])
+def test_norm_modulate(hidden, kind):
+    rows = 1000
+    g = torch.Generator(device=dev).manual_seed(hidden)
+    x = torch.randn(rows, hidden, device=dev, generator=g) * 3 + 1
+    shift = torch.randn(hidden, device=dev, generator=g)
+    scale = torch.randn(hidden, device=dev, generator=g) * 0.5
+    out = torch.empty(rows, hidden, device=dev, dtype=torch.bfloat16)
+    ops.norm_modulate(x, shift, scale, out, eps=1e-6, kind=kind)
+    if kind == 0:
+        exp = ref.modulate(x.cpu(), shift.cpu(), scale.cpu(), 1e-6)
+    else:
+        exp = x.cpu() * torch.rsqrt(x.cpu().pow(2).mean(-1, keepdim=True) + 1e-6) * (1 + scale.cpu()) + shift.cpu()
+    assert rel_l2(out, exp) < 5e-3
+
+
+def test_norm_modulate_probe():
+    rows, hidden = 513, 256
+    g = torch.Generator(device=dev).manual_seed(3)
+    x = torch.randn(rows, hidden, device=dev, generator=g)
+    prev = torch.randn(rows, hidden, device=dev, generator=g)
+    prev0 = prev.clone()
+    partials = torch.empty(2 * rows, device=dev)
+    out = torch.empty(rows, hidden, device=dev, dtype=torch.bfloat16)
+    ops.norm_modulate(x, None, None, out, probe_prev=prev, probe_partials=partials)
+    m = ref.layer_norm(x.cpu(), 1e-6)
+    sums = torch.empty(2, device=dev)
+    ops.rel_l1_reduce(partials, rows, sums)
+    exp_d = (m - prev0.cpu()).abs().sum()
+    exp_p = prev0.cpu().abs().sum()
+    assert abs(float(sums[0]) - float(exp_d)) / float(exp_d) < 1e-5
+    assert abs(float(sums[1]) - float(exp_p)) / float(exp_p) < 1e-5
+    assert rel_l2(prev, m) < 1e-6
+
+
+@pytest.mark.parametrize("d", [32, 64, 128])
+def test_qk_norm_rope_inplace(d):
+    heads, grid = 3, (2, 4, 6)
+    S = grid[0] * grid[1] * grid[2]
+    St = 5  # trailing text rows: no rope
+    rows = S + St
+    dims = (d - 2 * ((d - (d // 4) // 2 * 2) // 2 // 2 * 2), (d - (d // 4) // 2 * 2) // 2 // 2 * 2,
+            (d - (d // 4) // 2 * 2) // 2 // 2 * 2)
+    ang = ref.rope_angles(grid, dims, 1000.0)
+    cos = torch.cos(ang).float().to(dev)
+    sin = torch.sin(ang).float().to(dev)
+    g = torch.Generator(device=dev).manual_seed(d)
+    qkv = torch.randn(rows, 3, heads, d, device=dev, generator=g).to(torch.bfloat16)
+    qw = 1 + 0.1 * torch.randn(d, device=dev, generator=g)
+    kw = 1 + 0.1 * torch.randn(d, device=dev, generator=g)
+    src = qkv.clone()
+    ops.qk_norm_rope(qkv.view(rows, -1), heads, d, qw, kw, 1e-6, cos, sin, 0, S)
+    x = src.float().cpu()
+    q = ref.rms_norm(x[:, 0], qw.cpu(), 1e-6)
+    k = ref.rms_norm(x[:, 1], kw.cpu(), 1e-6)
+    q = torch.cat([ref.apply_rope(q[:S], ang), q[S:]])
+    k = torch.cat([ref.apply_rope(k[:S], ang), k[S:]])
+    assert rel_l2(qkv[:, 0], q) < 5e-3
+    assert rel_l2(qkv[:, 1], k) < 5e-3
+    assert torch.equal(qkv[:, 2], src[:, 2])
+
+
+def test_gemv_and_timestep_features():
+    n, k = 777, 256
+    g = torch.Generator(device=dev).manual_seed(5)
+    w = (torch.randn(n, k, device=dev, generator=g) * 0.1).to(torch.bfloat16)
+    b = torch.randn(n, device=dev, generator=g)
+    add = torch.randn(n, device=dev, generator=g)
+    x = torch.randn(k, device=dev, generator=g)
+    y = torch.empty(n, device=dev)
+    ops.gemv(w, x, y, bias=b, add=add, in_silu=True)
+    exp = w.float().cpu() @ torch.nn.functional.silu(x.cpu()) + b.cpu() + add.cpu()
+    assert rel_l2(y, exp) < 1e-5
+    t = torch.tensor([0.37], device=dev)
+    ops.gemv(w, None, y, bias=b, t=t)
+    exp = w.float().cpu() @ ref.timestep_features(0.37, k) + b.cpu()
+    assert rel_l2(y, exp) < 1e-4
+
+
+def test_patchify_roundtrip():
+    C, grid, patch = 8, (3, 4, 5), (1, 2, 2)
+    lat = torch.randn(C, 3, 8, 10, device=dev)
+    S = 3 * 4 * 5
+    tok = torch.empty(S, 32, device=dev)
+    tokb = torch.empty(S, 32, device=dev, dtype=torch.bfloat16)
+    ops.patchify(lat, tok, tokb, grid, patch)
+    assert torch.equal(tok.cpu(), ref.patchify(lat.cpu(), patch))
+    back = torch.empty_like(lat)
+    ops.unpatchify(tok, back, grid, patch)
+    assert torch.equal(back, lat)
+
+
+def test_cache_decide_matches_policy():
+    from paper_2505_10584_b200.schedule import RelL1Policy
+
+    pol = RelL1Policy(threshold=0.15, warmup=2)
+    rels = [0.0, 0.3, 0.05, 0.05, 0.07, 0.01, 0.2, 0.02, 0.03, 0.04]
+    state = torch.zeros(4, dtype=torch.int32, device=dev)
+    flags = torch.zeros(len(rels), dtype=torch.int32, device=dev)
+    relo = torch.zeros(len(rels), device=dev)
+    sums = torch.empty(2, device=dev)
+    acc, exp_flags = 0.0, []
+    for i, r in enumerate(rels):
+        sums.copy_(torch.tensor([r * 1000.0, 1000.0]))
+        ops.cache_decide(sums, state, pol.threshold, pol.warmup, len(rels), pol.force_last, flags, relo)
+        full, acc = pol.decide(i + 1, len(rels), acc, r)
+        exp_flags.append(int(full))
+    assert flags.cpu().tolist() == exp_flags
+
+
+def test_heads_to_seq():
+    P, rows, w = 4, 37, 64
+    src = torch.randn(P, rows, w, device=dev).to(torch.bfloat16)
+    dst = torch.empty(rows, P * w, device=dev, dtype=torch.bfloat16)
+    ops.heads_to_seq(src, rows, P, w, dst)
+    assert torch.equal(dst, src.permute(1, 0, 2).reshape(rows, P * w))
