@@ -43,7 +43,7 @@ int aqb_sm_count(void);
 /* ---------------------------------------------------------------------------
  * "LayerNorm + Scale/Shift" (memory.py:104):
  *   y[i,:] = bf16( norm(x[i,:]) * (1 + scale) + shift )
- * norm_kind 0 = LayerNorm (no affine), 1 = RMSNorm (no affine).
+ * norm_kind 0 = LayerNorm (no affine), 1 = RMSNorm (no affine), 2 = none (cast).
  * x f32 [rows, hidden] (stride ldx); y bf16 (stride ldy); shift/scale f32
  * [hidden] or NULL.  hidden % 128 == 0, hidden <= 4096.
  * Optional rel-L1 probe (diffusion cache, north_star): when probe_prev != NULL
@@ -80,13 +80,14 @@ int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t ldw, void* 
 
 /* ---------------------------------------------------------------------------
  * "Fused QKNorm" (memory.py:103) + 3D RoPE
- * + Ulysses pack.  src bf16 [rows, 3, heads, D] (row stride ld_src).  For each
- * row r and head h in [head_begin, head_begin + head_count):
- *   q = rms(q) * q_w, k = rms(k) * k_w; if (rope_row0 + r) < rope_rows:
- *   rotate interleaved pairs of q and k by rope_cos/sin[rope_row0 + r, :]
- *   (f32 [rope_rows, D/2]); v copied.
- * dst element (r, which, h, d) lives at
- *   dst + (j / hpg) * dst_group_stride + r * dst_row_stride + which * dst_which_stride
+ * + Ulysses pack.  src bf16 [rows, parts, heads, D] (row stride ld_src), parts
+ * in {1,2,3} (q | k,v | q,k,v).  For each row r and head h in
+ * [head_begin, head_begin + head_count): part p < norm_parts is RMS-normed
+ * with weight (p == 0 ? q_w : k_w) [D] and, if (rope_row0 + r) < rope_rows,
+ * its interleaved pairs are rotated by rope_cos/sin[rope_row0 + r, :]
+ * (f32 [rope_rows, D/2]); parts >= norm_parts are copied.
+ * dst element (r, part, h, d) lives at
+ *   dst + (j / hpg) * dst_group_stride + r * dst_row_stride + part * dst_which_stride
  *       + (j % hpg) * D + d,   j = h - head_begin, hpg = heads per group.
  * In place (dst == src, natural strides) is allowed.  D in {32, 64, 128, 256}.
  */
@@ -94,7 +95,7 @@ int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t head
                      int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
                      const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows, void* dst,
                      int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride, int32_t hpg,
-                     const int32_t* run_flag, int32_t run_if, void* stream);
+                     int32_t parts, int32_t norm_parts, const int32_t* run_flag, int32_t run_if, void* stream);
 
 /* ---------------------------------------------------------------------------
  * "Flash Attention" (memory.py:97): non-causal softmax(QK^T*scale)V

@@ -26,7 +26,7 @@ SIGNATURES = {
     "aqb_gemm_bf16": (c_int, [P, c_int64, P, c_int64, P, c_int64, c_int64, c_int64, c_int64, P, P, c_int32, P, P,
                               c_int64, P, c_int32, P]),
     "aqb_qk_norm_rope": (c_int, [P, c_int64, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, c_float, P, P, c_int64,
-                                 c_int64, P, c_int64, c_int64, c_int64, c_int32, P, c_int32, P]),
+                                 c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, P, c_int32, P]),
     "aqb_attention_fwd": (c_int, [P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64,
                                   c_int64, c_int64, c_int32, c_int32, c_float, P, c_int32, P]),
     "aqb_gemv": (c_int, [P, P, P, P, P, P, c_int64, c_int64, c_int32, P]),

@@ -52,13 +52,16 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
     for (int j = 0; j < NV; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
     mean = warp_sum(s) * (1.f / H);
   }
-  float ss = 0.f;
+  float rstd = 1.f;
+  if (kind != 2) {
+    float ss = 0.f;
 #pragma unroll
-  for (int j = 0; j < NV; ++j) {
-    const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
-    ss += (a * a + b * b) + (c * c + d * d);
+    for (int j = 0; j < NV; ++j) {
+      const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
+      ss += (a * a + b * b) + (c * c + d * d);
+    }
+    rstd = rsqrtf(warp_sum(ss) * (1.f / H) + eps);
   }
-  const float rstd = rsqrtf(warp_sum(ss) * (1.f / H) + eps);
   const float4* sh4 = reinterpret_cast<const float4*>(shift);
   const float4* sc4 = reinterpret_cast<const float4*>(scale);
   __nv_bfloat16* yr = y + row * ldy;
@@ -99,7 +102,7 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(
     const __nv_bfloat16* __restrict__ src, int64_t ld_src, int64_t rows, int heads, int head_begin, int head_count,
     const float* __restrict__ qw, const float* __restrict__ kw, float eps, const float* __restrict__ rcos,
     const float* __restrict__ rsin, int64_t rope_row0, int64_t rope_rows, __nv_bfloat16* dst, int64_t g_stride,
-    int64_t r_stride, int64_t w_stride, int hpg, const int32_t* flag, int32_t run_if) {
+    int64_t r_stride, int64_t w_stride, int hpg, int parts, int norm_parts, const int32_t* flag, int32_t run_if) {
   if (!gate_open(flag, run_if)) return;
   constexpr int NP = (D / 2 + 31) / 32;  // pairs per lane
   const int lane = threadIdx.x & 31;
@@ -112,8 +115,8 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(
   __nv_bfloat16* d = dst + static_cast<int64_t>(j / hpg) * g_stride + r * r_stride + static_cast<int64_t>(j % hpg) * D;
   const int64_t grow = rope_row0 + r;
   const bool rope = grow < rope_rows;
-#pragma unroll
-  for (int which = 0; which < 3; ++which) {
+#pragma unroll 1
+  for (int which = 0; which < parts; ++which) {
     const __nv_bfloat162* sp =
         reinterpret_cast<const __nv_bfloat162*>(s + static_cast<int64_t>(which) * heads * D + static_cast<int64_t>(h) * D);
     float2 e[NP];
@@ -124,7 +127,7 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(
       e[i] = (p < D / 2) ? __bfloat1622float2(sp[p]) : make_float2(0.f, 0.f);
       ss += e[i].x * e[i].x + e[i].y * e[i].y;
     }
-    if (which < 2) {
+    if (which < norm_parts) {
       const float rstd = rsqrtf(warp_sum(ss) * (1.f / D) + eps);
       const float* w = which == 0 ? qw : kw;
 #pragma unroll
@@ -349,7 +352,7 @@ extern "C" int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift
   AQB_CHECK_ARG(hidden % 128 == 0 && hidden >= 128 && hidden <= 4096, "norm_modulate: hidden %d unsupported", hidden);
   AQB_CHECK_ARG(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= hidden && ldy >= hidden, "norm_modulate: bad strides");
   AQB_CHECK_ARG(!probe_prev || probe_partials, "norm_modulate: probe needs partials");
-  AQB_CHECK_ARG(norm_kind == 0 || norm_kind == 1, "norm_modulate: bad kind");
+  AQB_CHECK_ARG(norm_kind >= 0 && norm_kind <= 2, "norm_modulate: bad kind");
   if (rows <= 0) return AQB_OK;
   const int grid = static_cast<int>((rows + 7) / 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
@@ -374,12 +377,17 @@ extern "C" int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, i
                                 int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
                                 const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows,
                                 void* dst, int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride,
-                                int32_t hpg, const int32_t* run_flag, int32_t run_if, void* stream) {
-  AQB_CHECK_ARG(src && dst && q_w && k_w, "qk_norm_rope: null pointer");
+                                int32_t hpg, int32_t parts, int32_t norm_parts, const int32_t* run_flag,
+                                int32_t run_if, void* stream) {
+  AQB_CHECK_ARG(src && dst, "qk_norm_rope: null pointer");
+  AQB_CHECK_ARG(parts >= 1 && parts <= 3 && norm_parts >= 0 && norm_parts <= parts && norm_parts <= 2,
+                "qk_norm_rope: bad parts");
+  AQB_CHECK_ARG(norm_parts < 1 || q_w, "qk_norm_rope: q_w missing");
+  AQB_CHECK_ARG(norm_parts < 2 || k_w, "qk_norm_rope: k_w missing");
   AQB_CHECK_ARG(head_begin >= 0 && head_count >= 1 && head_begin + head_count <= heads, "qk_norm_rope: bad heads");
   AQB_CHECK_ARG(hpg >= 1 && head_count % hpg == 0, "qk_norm_rope: bad heads-per-group");
   AQB_CHECK_ARG(rope_rows <= 0 || (rope_cos && rope_sin), "qk_norm_rope: rope tables missing");
-  AQB_CHECK_ARG(ld_src >= 3ll * heads * head_dim, "qk_norm_rope: bad ld_src");
+  AQB_CHECK_ARG(ld_src >= int64_t(parts) * heads * head_dim, "qk_norm_rope: bad ld_src");
   if (rows <= 0) return AQB_OK;
   const int64_t items = rows * head_count;
   const int grid = static_cast<int>((items + 7) / 8);
@@ -390,7 +398,8 @@ extern "C" int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, i
   case D:                                                                                                         \
     qk_norm_rope_kernel<D><<<grid, 256, 0, s>>>(sp, ld_src, rows, heads, head_begin, head_count, q_w, k_w, eps,   \
                                                 rope_cos, rope_sin, rope_row0, rope_rows, dp, dst_group_stride,   \
-                                                dst_row_stride, dst_which_stride, hpg, run_flag, run_if);         \
+                                                dst_row_stride, dst_which_stride, hpg, parts, norm_parts, run_flag,    \
+                                                run_if);                                                          \
     break;
   switch (head_dim) {
     QK_CASE(32) QK_CASE(64) QK_CASE(128) QK_CASE(256)

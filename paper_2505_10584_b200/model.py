@@ -1,0 +1,446 @@
+"""Single-DiT and MM-DiT denoise step on hand-written sm_100a kernels.
+
+Model construction mirrors the paper's two families (``PAPER.md:15-17,103,
+106``); every tensor op of a step is a libaqb.so kernel launched on the
+current stream (see ``ops.py``):
+
+Single-DiT block (AdaLN-single, PixArt layout)::
+
+    m   = norm_modulate(x, shift1, scale1)                  [HBM-bound]
+    qkv = gemm(m, Wqkv) (+bias)                             [tcgen05]
+    qkv = qk_norm_rope(qkv)  (in place / Ulysses pack)      [HBM-bound]
+    o   = attention(q, k, v)  (3D full, non-causal)         [tcgen05 + TMEM]
+    x  += gate1 * gemm(o, Wproj)                            [tcgen05, gate·residual epilogue]
+    x  += gemm(attention(qk_norm(gemm(x, Wq)), textK, textV), Wxproj)
+    x  += gate2 * gemm(gelu(gemm(norm_modulate(x), W1)), W2)
+
+MM-DiT runs the video and text streams as two row ranges of one residual
+buffer ``x = [video; text]``, so the joint attention over the concatenated
+sequence needs no concat copy; dual blocks use per-stream weights, single
+blocks one weight set over all rows.
+
+Diffusion cache (``dit-layer-cache``): the front
+``ceil(fraction·L)`` blocks always run; on a full step the rear blocks'
+offset ``x_out - x_in`` (video rows) is stored, on a cached step it is added
+instead of running them.  ``mode='dynamic'`` takes the decision on device
+(rel-L1 probe fused into block 0's norm kernel) and gates the rear kernels
+with a device flag — no host round-trip.
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import torch
+
+from . import ops
+from .config import DiTConfig
+from .errors import ConfigError
+from .parallel import Ulysses
+from .schedule import front_block_count
+from .weights import init_weights
+
+BF16, F32 = torch.bfloat16, torch.float32
+
+
+def rope_tables(grid, dims, theta, device):
+    """cos/sin [S, D/2] of the 3D RoPE (interleaved pairs, t|h|w channel split).
+
+    Setup-time table (once per geometry); the per-step rotation runs in
+    ``aqb_qk_norm_rope``.  Computed in float64 then rounded to fp32.
+    """
+    T, H, W = grid
+    tt, hh, ww = torch.meshgrid(torch.arange(T, device=device), torch.arange(H, device=device),
+                                torch.arange(W, device=device), indexing="ij")
+    pos = [tt.reshape(-1).double(), hh.reshape(-1).double(), ww.reshape(-1).double()]
+    ang = []
+    for p, d in zip(pos, dims):
+        j = torch.arange(0, d, 2, dtype=torch.float64, device=device)
+        ang.append(p[:, None] * (theta ** (-j / d))[None, :])
+    ang = torch.cat(ang, dim=1)
+    return torch.cos(ang).float().contiguous(), torch.sin(ang).float().contiguous()
+
+
+@dataclass
+class _Geometry:
+    grid: tuple
+    Sv: int        # video tokens (global)
+    Sv_loc: int    # video tokens on this rank
+    St: int        # text tokens (MM-DiT joint rows; 0 for Single-DiT)
+    rows: int      # rows of the residual buffer on this rank
+
+
+class DiTModel:
+    """Executable DiT (either family) bound to one GPU / one Ulysses rank."""
+
+    def __init__(self, cfg: DiTConfig, weights: dict | None = None, seed: int = 0, device="cuda",
+                 sp: Ulysses | None = None, cached_cost_fraction: float = 0.25):
+        if not torch.cuda.is_available():
+            raise ConfigError("a CUDA device is required (no CPU fallback)", "device")
+        self.cfg = cfg
+        self.device = torch.device(device)
+        self.sp = sp
+        if weights is None:
+            weights = init_weights(cfg, seed=seed, device=self.device)
+        self.W = {k: v.to(self.device).contiguous() for k, v in weights.items()}
+        self.n_front = front_block_count(cfg.num_layers, cached_cost_fraction)
+        self._stack_modulation()
+        self.geo = None
+
+    # ------------------------------------------------------------------ setup
+    def _stack_modulation(self):
+        cfg, W, H = self.cfg, self.W, self.cfg.hidden_size
+        if cfg.family == "single-dit":
+            self.tables = torch.stack([W[f"blocks.{i}.table"] for i in range(cfg.num_single)]).contiguous()
+            return
+        names = []
+        for i in range(cfg.num_dual):
+            names += [f"dual.{i}.img.mod", f"dual.{i}.txt.mod"]
+        names += [f"single.{i}.mod" for i in range(cfg.num_single)]
+        names += ["final.mod"]
+        self.mod_names = names
+        self.mod_w = torch.cat([W[f"{n}.w"] for n in names]).contiguous()
+        self.mod_b = torch.cat([W[f"{n}.b"] for n in names]).contiguous()
+        off, self.mod_off = 0, {}
+        for n in names:
+            self.mod_off[n] = off
+            off += W[f"{n}.b"].numel()
+        for n in names:  # the stacked copy is the only one kept
+            del W[f"{n}.w"]
+
+    def prepare(self, grid, text: torch.Tensor, pooled: torch.Tensor | None = None):
+        """Bind geometry + conditioning; allocate the step workspace."""
+        cfg, dev = self.cfg, self.device
+        grid = tuple(int(g) for g in grid)
+        Sv = grid[0] * grid[1] * grid[2]
+        P = 1 if self.sp is None else self.sp.P
+        if self.sp is not None:
+            self.sp.check(cfg.num_heads, Sv)
+        Sv_loc = Sv // P
+        St = cfg.text_len if cfg.family == "mm-dit" else 0
+        if text.shape != (cfg.text_len, cfg.text_dim):
+            raise ConfigError(f"text must be [{cfg.text_len}, {cfg.text_dim}]", "inputs.text")
+        self.geo = _Geometry(grid, Sv, Sv_loc, St, Sv_loc + St)
+        H, F, A, D = cfg.hidden_size, cfg.ffn_dim, cfg.num_heads, cfg.head_dim
+        rows = self.geo.rows
+        e = lambda *s, dt=BF16: torch.empty(*s, device=dev, dtype=dt)  # noqa: E731
+        self.x = e(rows, H, dt=F32)
+        self.m = e(rows, H)
+        self.qkv = e(rows, 3 * H)
+        self.o = e(rows, H)
+        self.h = e(rows, F)
+        self.lat = e(Sv_loc, cfg.patch_dim, dt=F32)
+        self.lat_bf = e(Sv_loc, cfg.patch_dim)
+        self.off = e(Sv_loc, H, dt=F32)
+        self.cos, self.sin = rope_tables(grid, cfg.rope_dims, cfg.rope_theta, dev)
+        # per-step scalars (t, dt) live on device so one captured step replays for every step
+        self.idx = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.cur = torch.zeros(2, device=dev, dtype=F32)
+        # cache probe / decision state
+        self.prev = torch.zeros(Sv_loc, H, device=dev, dtype=F32)
+        self.partials = e(2 * Sv_loc, dt=F32)
+        self.sums = e(2, dt=F32)
+        self.cstate = torch.zeros(4, device=dev, dtype=torch.int32)
+        self.flag = self.cstate[1:2]
+        t_bf = text.to(dev, F32).to(BF16).contiguous()
+        W = self.W
+        if cfg.family == "single-dit":
+            self.t0 = e(H, dt=F32)
+            self.th = e(H, dt=F32)
+            self.tmod = e(6 * H, dt=F32)
+            self.mods = e(cfg.num_single, 6 * H, dt=F32)
+            self.fmods = e(2 * H, dt=F32)
+            self.xq = e(Sv_loc, H)
+            # step-independent cross-attention K/V of the text, once per call (K RMS-normed)
+            self.text_kv = []
+            for i in range(cfg.num_single):
+                kv = e(cfg.text_len, 2 * H)
+                ops.gemm(t_bf, W[f"blocks.{i}.xkv.w"], kv, bias=W[f"blocks.{i}.xkv.b"])
+                ops.qk_norm_rope(kv, A, D, W[f"blocks.{i}.xk_norm"], None, cfg.qk_norm_eps, parts=2, norm_parts=1)
+                self.text_kv.append(kv)
+        else:
+            if pooled is None or pooled.shape != (cfg.pooled_dim,):
+                raise ConfigError(f"pooled must be [{cfg.pooled_dim}]", "inputs.pooled")
+            self.th = e(H, dt=F32)
+            self.vec = e(H, dt=F32)
+            self.pe = e(H, dt=F32)
+            pl = pooled.to(dev, F32).contiguous()
+            ops.gemv(W["p_emb.fc1.w"], pl, self.th, bias=W["p_emb.fc1.b"])
+            ops.gemv(W["p_emb.fc2.w"], self.th, self.pe, bias=W["p_emb.fc2.b"], in_silu=True)
+            self.allmods = e(self.mod_w.shape[0], dt=F32)
+            self.txt0 = e(St, H, dt=F32)
+            ops.gemm(t_bf, W["txt_in.w"], self.txt0, bias=W["txt_in.b"], epilogue="f32")
+        if self.sp is not None and self.sp.P > 1:
+            hl = A // P
+            self.hl = hl
+            self.a2a_snd = e(P, Sv_loc, 3, hl, D)
+            self.a2a_rcv = e(Sv + St, 3, hl, D)
+            self.oh = e(Sv + St, hl * D)
+            self.ob = e(P, Sv_loc, hl * D)
+            if St:
+                self.tg = e(P, St, hl * D)
+        return self
+
+    # ------------------------------------------------------------- primitives
+    def _mod(self, name):
+        H = self.cfg.hidden_size
+        if self.cfg.family == "single-dit":
+            i = name
+            row = self.mods[i]
+            return [row[k * H:(k + 1) * H] for k in range(6)]
+        o = self.mod_off[name]
+        n = 2 if name == "final.mod" else 6
+        return [self.allmods[o + k * H:o + (k + 1) * H] for k in range(n)]
+
+    def _attention_self(self, p, r0, r1, rope, flag, run_if, txt=None):
+        """QK-norm/RoPE + joint self-attention over rows [r0, r1) (+ text rows for MM-DiT).
+
+        P == 1: in place on ``qkv``.  P > 1: Ulysses pack -> all-to-all ->
+        attention over A/P heads -> all-to-all back -> head->sequence repack.
+        ``p`` = weight prefix of the video (or only) stream, ``txt`` = text
+        stream prefix (dual blocks) or the same prefix (single blocks).
+        """
+        cfg, g, W = self.cfg, self.geo, self.W
+        A, D, H, eps = cfg.num_heads, cfg.head_dim, cfg.hidden_size, cfg.qk_norm_eps
+        Sv_loc, St = g.Sv_loc, g.St
+        if self.sp is None or self.sp.P == 1:
+            qv = self.qkv[r0:Sv_loc]
+            ops.qk_norm_rope(qv, A, D, W[f"{p}.q_norm"], W[f"{p}.k_norm"], eps, self.cos, self.sin, 0, g.Sv,
+                             run_flag=flag, run_if=run_if)
+            if St:
+                tp = txt or p
+                ops.qk_norm_rope(self.qkv[Sv_loc:], A, D, W[f"{tp}.q_norm"], W[f"{tp}.k_norm"], eps,
+                                 run_flag=flag, run_if=run_if)
+            q = self.qkv[r0:r1]
+            ops.attention(q, q[:, H:], q[:, 2 * H:], self.o[r0:r1], A, D, run_flag=flag, run_if=run_if)
+            return
+        sp, P, hl = self.sp, self.sp.P, self.hl
+        snd, rcv = self.a2a_snd, self.a2a_rcv
+        ops.qk_norm_rope(self.qkv[:Sv_loc], A, D, W[f"{p}.q_norm"], W[f"{p}.k_norm"], eps, self.cos, self.sin,
+                         sp.rank * Sv_loc, g.Sv, dst=snd, hpg=hl, dst_group_stride=Sv_loc * 3 * hl * D,
+                         dst_row_stride=3 * hl * D, dst_which_stride=hl * D, run_flag=flag, run_if=run_if)
+        sp.all_to_all(rcv[:g.Sv].view(-1), snd.view(-1))
+        if St:
+            tp = txt or p
+            ops.qk_norm_rope(self.qkv[Sv_loc:], A, D, W[f"{tp}.q_norm"], W[f"{tp}.k_norm"], eps,
+                             dst=rcv[g.Sv:].view(St, -1), head_begin=sp.rank * hl, head_count=hl, hpg=hl,
+                             dst_row_stride=3 * hl * D, dst_which_stride=hl * D, run_flag=flag, run_if=run_if)
+        q = rcv.view(g.Sv + St, -1)
+        ops.attention(q, q[:, hl * D:], q[:, 2 * hl * D:], self.oh, hl, D, run_flag=flag, run_if=run_if)
+        sp.all_to_all(self.ob.view(-1), self.oh[:g.Sv].reshape(-1))
+        ops.heads_to_seq(self.ob, Sv_loc, P, hl * D, self.o[:Sv_loc], run_flag=flag, run_if=run_if)
+        if St:
+            sp.all_gather(self.tg.view(-1), self.oh[g.Sv:].reshape(-1))
+            ops.heads_to_seq(self.tg, St, P, hl * D, self.o[Sv_loc:], run_flag=flag, run_if=run_if)
+
+    def _mlp(self, p, r0, r1, mods, flag, run_if):
+        """x += gate2 * fc2(gelu(fc1(norm_mod(x, shift2, scale2))))  on rows [r0, r1)."""
+        W, eps = self.W, self.cfg.norm_eps
+        x, m, h = self.x[r0:r1], self.m[r0:r1], self.h[r0:r1]
+        ops.norm_modulate(x, mods[3], mods[4], m, eps, run_flag=flag, run_if=run_if)
+        ops.gemm(m, W[f"{p}.fc1.w"], h, bias=W[f"{p}.fc1.b"], epilogue="gelu", run_flag=flag, run_if=run_if)
+        ops.gemm(h, W[f"{p}.fc2.w"], x, bias=W[f"{p}.fc2.b"], gate=mods[5], epilogue="gate_res", run_flag=flag,
+                 run_if=run_if)
+
+    # ----------------------------------------------------------------- blocks
+    def _single_dit_block(self, i, flag, run_if, probe):
+        cfg, g, W = self.cfg, self.geo, self.W
+        A, D, H, eps = cfg.num_heads, cfg.head_dim, cfg.hidden_size, cfg.norm_eps
+        p = f"blocks.{i}"
+        mods = self._mod(i)
+        n = g.Sv_loc
+        ops.norm_modulate(self.x, mods[0], mods[1], self.m, eps, probe_prev=self.prev if probe else None,
+                          probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
+        if probe:
+            self._decide()
+        ops.gemm(self.m, W[f"{p}.qkv.w"], self.qkv, bias=W[f"{p}.qkv.b"], run_flag=flag, run_if=run_if)
+        self._attention_self(p, 0, n, True, flag, run_if)
+        ops.gemm(self.o, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=mods[2], epilogue="gate_res",
+                 run_flag=flag, run_if=run_if)
+        # cross-attention to the text (no norm before it, PixArt-α); K/V precomputed per call
+        ops.norm_modulate(self.x, None, None, self.m, eps, kind=2, run_flag=flag, run_if=run_if)
+        ops.gemm(self.m, W[f"{p}.xq.w"], self.xq, bias=W[f"{p}.xq.b"], run_flag=flag, run_if=run_if)
+        ops.qk_norm_rope(self.xq, A, D, W[f"{p}.xq_norm"], None, cfg.qk_norm_eps, parts=1, norm_parts=1,
+                         run_flag=flag, run_if=run_if)
+        kv = self.text_kv[i]
+        ops.attention(self.xq, kv, kv[:, H:], self.o, A, D, run_flag=flag, run_if=run_if)
+        ops.gemm(self.o, W[f"{p}.xproj.w"], self.x, bias=W[f"{p}.xproj.b"], epilogue="gate_res", run_flag=flag,
+                 run_if=run_if)
+        self._mlp(p, 0, n, mods, flag, run_if)
+
+    def _mm_dual_block(self, i, flag, run_if, probe):
+        cfg, g, W, eps = self.cfg, self.geo, self.W, self.cfg.norm_eps
+        n, R = g.Sv_loc, g.rows
+        pi, pt = f"dual.{i}.img", f"dual.{i}.txt"
+        mi, mt = self._mod(f"{pi}.mod"), self._mod(f"{pt}.mod")
+        ops.norm_modulate(self.x[:n], mi[0], mi[1], self.m[:n], eps, probe_prev=self.prev if probe else None,
+                          probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
+        if probe:
+            self._decide()
+        ops.norm_modulate(self.x[n:], mt[0], mt[1], self.m[n:], eps, run_flag=flag, run_if=run_if)
+        ops.gemm(self.m[:n], W[f"{pi}.qkv.w"], self.qkv[:n], bias=W[f"{pi}.qkv.b"], run_flag=flag, run_if=run_if)
+        ops.gemm(self.m[n:], W[f"{pt}.qkv.w"], self.qkv[n:], bias=W[f"{pt}.qkv.b"], run_flag=flag, run_if=run_if)
+        self._attention_self(pi, 0, R, True, flag, run_if, txt=pt)
+        ops.gemm(self.o[:n], W[f"{pi}.proj.w"], self.x[:n], bias=W[f"{pi}.proj.b"], gate=mi[2], epilogue="gate_res",
+                 run_flag=flag, run_if=run_if)
+        ops.gemm(self.o[n:], W[f"{pt}.proj.w"], self.x[n:], bias=W[f"{pt}.proj.b"], gate=mt[2], epilogue="gate_res",
+                 run_flag=flag, run_if=run_if)
+        self._mlp(pi, 0, n, mi, flag, run_if)
+        self._mlp(pt, n, R, mt, flag, run_if)
+
+    def _mm_single_block(self, i, flag, run_if, probe):
+        cfg, g, W, eps = self.cfg, self.geo, self.W, self.cfg.norm_eps
+        n, R = g.Sv_loc, g.rows
+        p = f"single.{i}"
+        md = self._mod(f"{p}.mod")
+        if probe:
+            ops.norm_modulate(self.x[:n], md[0], md[1], self.m[:n], eps, probe_prev=self.prev,
+                              probe_partials=self.partials, run_flag=flag, run_if=run_if)
+            self._decide()
+            ops.norm_modulate(self.x[n:], md[0], md[1], self.m[n:], eps, run_flag=flag, run_if=run_if)
+        else:
+            ops.norm_modulate(self.x, md[0], md[1], self.m, eps, run_flag=flag, run_if=run_if)
+        ops.gemm(self.m, W[f"{p}.qkv.w"], self.qkv, bias=W[f"{p}.qkv.b"], run_flag=flag, run_if=run_if)
+        self._attention_self(p, 0, R, True, flag, run_if)
+        ops.gemm(self.o, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=md[2], epilogue="gate_res",
+                 run_flag=flag, run_if=run_if)
+        self._mlp(p, 0, R, md, flag, run_if)
+
+    def _block(self, i, flag, run_if, probe):
+        cfg = self.cfg
+        if cfg.family == "single-dit":
+            return self._single_dit_block(i, flag, run_if, probe)
+        if i < cfg.num_dual:
+            return self._mm_dual_block(i, flag, run_if, probe)
+        return self._mm_single_block(i - cfg.num_dual, flag, run_if, probe)
+
+    # ------------------------------------------------------------------ steps
+    def reset(self, x0: torch.Tensor, num_steps: int, policy=None):
+        """Load the initial latent [C, T, H, W] and the Euler grid t_i = i/N."""
+        cfg, g = self.cfg, self.geo
+        if g is None:
+            raise ConfigError("call prepare() first", "model")
+        C = cfg.latent_channels
+        pt, ph, pw = cfg.patch
+        exp = (C, g.grid[0] * pt, g.grid[1] * ph, g.grid[2] * pw)
+        if tuple(x0.shape) != exp:
+            raise ConfigError(f"latent must be {exp}, got {tuple(x0.shape)}", "inputs.x0")
+        dev = self.device
+        full_tok = torch.empty(g.Sv, cfg.patch_dim, device=dev, dtype=F32)
+        lat = x0.to(dev, F32, non_blocking=True).contiguous()
+        ops.patchify(lat, full_tok, None, g.grid, cfg.patch)
+        r = 0 if self.sp is None else self.sp.rank
+        self.lat.copy_(full_tok[r * g.Sv_loc:(r + 1) * g.Sv_loc])
+        self.lat_bf.copy_(self.lat)
+        self.num_steps = num_steps
+        self.ts = torch.arange(num_steps, device=dev, dtype=torch.float64).div(num_steps).float()
+        self.dts = torch.full((num_steps,), 1.0 / num_steps, device=dev, dtype=F32)
+        self.idx.zero_()
+        self.cstate.zero_()
+        self.prev.zero_()
+        self.policy = policy
+        self.flags_out = torch.zeros(num_steps, device=dev, dtype=torch.int32)
+        self.rels_out = torch.zeros(num_steps, device=dev, dtype=F32)
+
+    def _decide(self):
+        pol = self.policy
+        ops.rel_l1_reduce(self.partials, self.geo.Sv_loc, self.sums)
+        if self.sp is not None and self.sp.P > 1:
+            self.sp.all_reduce_sum(self.sums)
+        ops.cache_decide(self.sums, self.cstate, pol.threshold, pol.warmup, self.num_steps, pol.force_last,
+                         self.flags_out, self.rels_out)
+
+    def _embed(self):
+        cfg, W, g = self.cfg, self.W, self.geo
+        ops.step_scalars(self.ts, self.dts, self.idx, self.cur)
+        t = self.cur[0:1]
+        ops.gemv(W["t_emb.fc1.w"], None, self.th, bias=W["t_emb.fc1.b"], t=t)
+        if cfg.family == "single-dit":
+            ops.gemv(W["t_emb.fc2.w"], self.th, self.t0, bias=W["t_emb.fc2.b"], in_silu=True)
+            ops.gemv(W["t_block.w"], self.t0, self.tmod, bias=W["t_block.b"], in_silu=True)
+            ops.add_bcast(self.mods.view(-1), self.tmod, self.tables.view(-1))
+            ops.add_bcast(self.fmods, self.t0, W["final.table"])
+        else:
+            ops.gemv(W["t_emb.fc2.w"], self.th, self.vec, bias=W["t_emb.fc2.b"], add=self.pe, in_silu=True)
+            ops.gemv(self.mod_w, self.vec, self.allmods, bias=self.mod_b, in_silu=True)
+        n = g.Sv_loc
+        ops.gemm(self.lat_bf, W["x_emb.w"], self.x[:n], bias=W["x_emb.b"], epilogue="f32")
+        if g.St:
+            self.x[n:].copy_(self.txt0)
+
+    def _final(self):
+        cfg, W, g = self.cfg, self.W, self.geo
+        n, H = g.Sv_loc, cfg.hidden_size
+        if cfg.family == "single-dit":
+            shift, scale = self.fmods[:H], self.fmods[H:]
+        else:
+            shift, scale = self._mod("final.mod")
+        ops.norm_modulate(self.x[:n], shift, scale, self.m[:n], cfg.norm_eps)
+        ops.gemm(self.m[:n], W["final.w"], self.lat, bias=W["final.b"], epilogue="euler", alpha=self.cur[1:2],
+                 aux=self.lat_bf)
+        ops.step_scalars(self.ts, self.dts, self.idx, self.cur, advance=True)
+
+    def step(self, mode: str = "full", use_cache: bool = True):
+        """Issue one denoise step (velocity + Euler update) on the current stream.
+
+        mode: ``full`` | ``cached`` (host-decided, static schedule) |
+        ``dynamic`` (device-decided with the rel-L1 policy set in reset()).
+        ``use_cache=False`` skips the offset bookkeeping (schedule without cached steps).
+        """
+        cfg = self.cfg
+        L, nf = cfg.num_layers, self.n_front
+        dyn = mode == "dynamic"
+        flag = self.flag if dyn else None
+        xi = self.x[:self.geo.Sv_loc]
+        self._embed()
+        cache = use_cache and nf < L
+        for i in range(L):
+            if i == nf and cache:
+                if mode == "cached":
+                    ops.cache_offset(xi, self.off, 2)
+                    break
+                if dyn:
+                    ops.cache_offset(xi, self.off, 2, run_flag=flag, run_if=0)
+                ops.cache_offset(xi, self.off, 0, run_flag=flag, run_if=1)
+            rear = i >= nf
+            self._block(i, flag if (dyn and rear) else None, 1, probe=(dyn and i == 0))
+        if cache and mode != "cached":
+            ops.cache_offset(xi, self.off, 1, run_flag=flag, run_if=1)
+        self._final()
+
+    def latent(self) -> torch.Tensor:
+        """Current latent [C, T, H, W] (gathered over Ulysses ranks)."""
+        cfg, g = self.cfg, self.geo
+        tok = self.lat
+        if self.sp is not None and self.sp.P > 1:
+            full = torch.empty(g.Sv, cfg.patch_dim, device=self.device, dtype=F32)
+            self.sp.all_gather(full.view(-1), self.lat.view(-1))
+            tok = full
+        pt, ph, pw = cfg.patch
+        out = torch.empty(cfg.latent_channels, g.grid[0] * pt, g.grid[1] * ph, g.grid[2] * pw, device=self.device,
+                          dtype=F32)
+        ops.unpatchify(tok, out, g.grid, cfg.patch)
+        return out
+
+
+class SingleDiT(DiTModel):
+    """Aquarius Single-DiT (2B): AdaLN-single + cross-attention."""
+
+    def __init__(self, cfg: DiTConfig, **kw):
+        if cfg.family != "single-dit":
+            raise ConfigError("SingleDiT needs a single-dit config", "model.family")
+        super().__init__(cfg, **kw)
+
+
+class MMDiT(DiTModel):
+    """Aquarius Multimodal-DiT (13.4B): dual-stream then joint blocks."""
+
+    def __init__(self, cfg: DiTConfig, **kw):
+        if cfg.family != "mm-dit":
+            raise ConfigError("MMDiT needs an mm-dit config", "model.family")
+        super().__init__(cfg, **kw)
+
+
+def build_model(cfg: DiTConfig, **kw) -> DiTModel:
+    return (SingleDiT if cfg.family == "single-dit" else MMDiT)(cfg, **kw)

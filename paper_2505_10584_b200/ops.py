@@ -66,8 +66,8 @@ def gemm(a, w, out, bias=None, gate=None, epilogue="bf16", alpha=None, aux=None,
 
 def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_row0=0, rope_rows=0,
                  dst=None, head_begin=0, head_count=None, hpg=None, dst_group_stride=0, dst_row_stride=None,
-                 dst_which_stride=None, run_flag=None, run_if=1):
-    """QK-RMSNorm + 3D RoPE over a [rows, 3, heads, D] QKV buffer (optionally repacked into dst)."""
+                 dst_which_stride=None, parts=3, norm_parts=2, run_flag=None, run_if=1):
+    """QK-RMSNorm + 3D RoPE over a [rows, parts, heads, D] buffer (optionally repacked into dst)."""
     _need(src, BF16, "qk_norm_rope.src")
     rows = src.shape[0]
     head_count = heads if head_count is None else head_count
@@ -80,8 +80,8 @@ def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_r
         dst_which_stride = heads * head_dim
     _native.call("aqb_qk_norm_rope", _p(src), src.stride(0), rows, heads, head_begin, head_count, head_dim,
                  _p(q_w), _p(k_w), float(eps), _p(cos), _p(sin), int(rope_row0), int(rope_rows), _p(dst),
-                 int(dst_group_stride), int(dst_row_stride), int(dst_which_stride), int(hpg), _p(run_flag),
-                 int(run_if), _stream())
+                 int(dst_group_stride), int(dst_row_stride), int(dst_which_stride), int(hpg), int(parts),
+                 int(norm_parts), _p(run_flag), int(run_if), _stream())
     return dst
 
 

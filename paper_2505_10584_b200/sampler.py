@@ -1,0 +1,98 @@
+"""Flow-matching Euler denoise loop with the diffusion cache.
+
+``denoise(model, x0, num_steps, cache)`` is the sampler entry point the
+north_star asks for (the reference has none; PAPER.md:127-131 gives the
+flow-matching formulation; uniform Euler grid t_i = i/N is the builder's
+choice).  ``cache`` is either
+
+* a :class:`CacheSchedule` (e.g. ``plan_cache(...)``) — consumed unchanged:
+  ``per_step_full[i]`` picks a full or a cached step on the host, so skipped
+  rear blocks are simply not launched; or
+* a :class:`RelL1Policy` — decided on device each step (no host sync);
+  the flags actually taken come back as ``DenoiseResult.schedule``; or
+* ``None`` — no cache (every step full).
+
+With ``graph=True`` each step kind is captured once as a CUDA graph and
+replayed (t / dt / step index live on device, so one graph serves every step).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import torch
+
+from .errors import ConfigError
+from .schedule import CacheSchedule, RelL1Policy, no_cache
+
+
+@dataclass
+class DenoiseResult:
+    latent: torch.Tensor                  # [C, T, H, W] f32 (device)
+    schedule: CacheSchedule               # flags actually taken
+    rel_l1: list = field(default_factory=list)  # per-step rel-L1 (dynamic policy)
+    trajectory: list = field(default_factory=list)
+
+
+class _Graphs:
+    def __init__(self):
+        self.g = {}
+
+    def run(self, model, mode, use_cache):
+        key = (mode, use_cache)
+        if key not in self.g:
+            # warm the kernels' one-time attribute setup outside capture
+            s = torch.cuda.Stream()
+            s.wait_stream(torch.cuda.current_stream())
+            g = torch.cuda.CUDAGraph()
+            saved = (model.idx.clone(), model.cur.clone(), model.cstate.clone(), model.prev.clone(),
+                     model.lat.clone(), model.lat_bf.clone(), model.off.clone(), model.flags_out.clone(),
+                     model.rels_out.clone())
+            with torch.cuda.stream(s):
+                model.step(mode, use_cache)  # warm-up (then state is restored)
+            torch.cuda.current_stream().wait_stream(s)
+            for dst, src in zip((model.idx, model.cur, model.cstate, model.prev, model.lat, model.lat_bf, model.off,
+                                 model.flags_out, model.rels_out), saved):
+                dst.copy_(src)
+            with torch.cuda.graph(g):
+                model.step(mode, use_cache)
+            self.g[key] = g
+        self.g[key].replay()
+
+
+def denoise(model, x0: torch.Tensor, num_steps: int, cache=None, trajectory: bool = False,
+            graph: bool = False, graphs: _Graphs | None = None) -> DenoiseResult:
+    """Run ``num_steps`` Euler steps from the noise latent ``x0`` [C, T, H, W]."""
+    if num_steps < 1:
+        raise ConfigError("num_steps must be >= 1", "sampler.num_steps")
+    if cache is None:
+        cache = no_cache(num_steps)
+    dynamic = isinstance(cache, RelL1Policy)
+    if not dynamic:
+        if not isinstance(cache, CacheSchedule):
+            raise ConfigError("cache must be a CacheSchedule, a RelL1Policy or None", "sampler.cache")
+        if cache.total_steps != num_steps:
+            raise ConfigError("schedule length != num_steps", "sampler.cache")
+        if cache.mode != "dit-layer-cache" and not all(cache.per_step_full):
+            raise ConfigError("only dit-layer-cache is executable in this release", "cache.mode")
+    model.reset(x0, num_steps, policy=cache if dynamic else None)
+    use_cache = dynamic or not all(cache.per_step_full)
+    traj = []
+    if graph and graphs is None:
+        graphs = _Graphs()
+    for i in range(num_steps):
+        mode = "dynamic" if dynamic else ("full" if cache.per_step_full[i] else "cached")
+        if graph:
+            graphs.run(model, mode, use_cache)
+        else:
+            model.step(mode, use_cache)
+        if trajectory:
+            traj.append(model.latent())
+    lat = model.latent()
+    if dynamic:
+        flags = [bool(f) for f in model.flags_out.tolist()]
+        rels = model.rels_out.tolist()
+        sched = cache.as_schedule(flags)
+    else:
+        sched, rels = cache, []
+    return DenoiseResult(latent=lat, schedule=sched, rel_l1=rels, trajectory=traj)
