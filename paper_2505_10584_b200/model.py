@@ -333,15 +333,23 @@ class DiTModel:
         r = 0 if self.sp is None else self.sp.rank
         self.lat.copy_(full_tok[r * g.Sv_loc:(r + 1) * g.Sv_loc])
         self.lat_bf.copy_(self.lat)
-        self.num_steps = num_steps
-        self.ts = torch.arange(num_steps, device=dev, dtype=torch.float64).div(num_steps).float()
-        self.dts = torch.full((num_steps,), 1.0 / num_steps, device=dev, dtype=F32)
+        if getattr(self, "num_steps", None) != num_steps:
+            # (re)allocate the per-step tables; captured CUDA graphs hold their addresses,
+            # so a new step count starts a new graph generation
+            self.num_steps = num_steps
+            self.ts = torch.empty(num_steps, device=dev, dtype=F32)
+            self.dts = torch.empty(num_steps, device=dev, dtype=F32)
+            self.flags_out = torch.empty(num_steps, device=dev, dtype=torch.int32)
+            self.rels_out = torch.empty(num_steps, device=dev, dtype=F32)
+            self.generation = getattr(self, "generation", 0) + 1
+        self.ts.copy_(torch.arange(num_steps, device=dev, dtype=torch.float64).div(num_steps))
+        self.dts.fill_(1.0 / num_steps)
+        self.flags_out.zero_()
+        self.rels_out.zero_()
         self.idx.zero_()
         self.cstate.zero_()
         self.prev.zero_()
         self.policy = policy
-        self.flags_out = torch.zeros(num_steps, device=dev, dtype=torch.int32)
-        self.rels_out = torch.zeros(num_steps, device=dev, dtype=F32)
 
     def _decide(self):
         pol = self.policy

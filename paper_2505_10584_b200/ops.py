@@ -21,6 +21,57 @@ def _stream():
     return torch.cuda.current_stream().cuda_stream
 
 
+class KernelProfiler:
+    """Optional per-launch CUDA-event timing / counting (bench.py).
+
+    When installed with :func:`set_profiler`, every kernel launch is
+    bracketed by CUDA events on the launching (current) stream and recorded
+    as ``(kind, start, end, work)`` where ``work`` is FLOPs for tensor-core
+    kernels and algorithmic HBM bytes for the memory-bound ones.  With
+    ``timing=False`` launches are only counted.
+    """
+
+    def __init__(self, timing: bool = True):
+        self.timing = timing
+        self.records = []
+        self.count = 0
+
+    def summary(self):
+        torch.cuda.synchronize()
+        out = {}
+        for kind, e0, e1, work in self.records:
+            d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "work": 0.0})
+            d["launches"] += 1
+            d["ms"] += e0.elapsed_time(e1)
+            d["work"] += work
+        return out
+
+
+_PROF: KernelProfiler | None = None
+
+
+def set_profiler(p: KernelProfiler | None):
+    global _PROF
+    _PROF = p
+
+
+def _run(kind, work, name, *args):
+    prof = _PROF
+    if prof is None:
+        _native.call(name, *args)
+        return
+    prof.count += 1
+    if not prof.timing:
+        _native.call(name, *args)
+        return
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    _native.call(name, *args)
+    e1.record()
+    prof.records.append((kind, e0, e1, float(work)))
+
+
 def _p(t):
     return None if t is None else t.data_ptr()
 
@@ -40,7 +91,7 @@ def norm_modulate(x, shift, scale, out, eps=1e-6, kind=0, probe_prev=None, probe
     _need(x, F32, "norm_modulate.x")
     _need(out, BF16, "norm_modulate.out")
     rows, hidden = x.shape
-    _native.call("aqb_norm_modulate", _p(x), x.stride(0), _p(shift), _p(scale), _p(out), out.stride(0), rows,
+    _run("norm_modulate", rows * hidden * (4 + 2) + (8 * rows * hidden if probe_prev is not None else 0), "aqb_norm_modulate", _p(x), x.stride(0), _p(shift), _p(scale), _p(out), out.stride(0), rows,
                  hidden, float(eps), int(kind), _p(probe_prev), _p(probe_partials), _p(run_flag), int(run_if),
                  _stream())
     return out
@@ -58,7 +109,7 @@ def gemm(a, w, out, bias=None, gate=None, epilogue="bf16", alpha=None, aux=None,
     _need(out, BF16 if e in (0, 1) else F32, "gemm.out")
     if out.shape[0] != m or out.shape[1] < n:
         raise NativeError(f"gemm: out shape {tuple(out.shape)} vs ({m},{n})")
-    _native.call("aqb_gemm_bf16", _p(a), a.stride(0), _p(w), w.stride(0), _p(out), out.stride(0), m, n, k,
+    _run("gemm", 2.0 * m * n * k, "aqb_gemm_bf16", _p(a), a.stride(0), _p(w), w.stride(0), _p(out), out.stride(0), m, n, k,
                  _p(bias), _p(gate), e, _p(alpha), _p(aux), aux.stride(0) if aux is not None else 0,
                  _p(run_flag), int(run_if), _stream())
     return out
@@ -78,7 +129,7 @@ def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_r
         dst_row_stride = dst.stride(0)
     if dst_which_stride is None:
         dst_which_stride = heads * head_dim
-    _native.call("aqb_qk_norm_rope", _p(src), src.stride(0), rows, heads, head_begin, head_count, head_dim,
+    _run("qk_norm_rope", 2 * rows * head_count * head_dim * parts * 2, "aqb_qk_norm_rope", _p(src), src.stride(0), rows, heads, head_begin, head_count, head_dim,
                  _p(q_w), _p(k_w), float(eps), _p(cos), _p(sin), int(rope_row0), int(rope_rows), _p(dst),
                  int(dst_group_stride), int(dst_row_stride), int(dst_which_stride), int(hpg), int(parts),
                  int(norm_parts), _p(run_flag), int(run_if), _stream())
@@ -92,7 +143,7 @@ def attention(q, k, v, o, heads, head_dim, q_head_stride=None, k_head_stride=Non
         _need(t, BF16, f"attention.{nm}")
     hs = lambda x: head_dim if x is None else x  # noqa: E731
     scale = head_dim ** -0.5 if scale is None else scale
-    _native.call("aqb_attention_fwd", _p(q), q.stride(0), hs(q_head_stride), _p(k), k.stride(0), hs(k_head_stride),
+    _run("attention", 4.0 * q.shape[0] * k.shape[0] * head_dim * heads, "aqb_attention_fwd", _p(q), q.stride(0), hs(q_head_stride), _p(k), k.stride(0), hs(k_head_stride),
                  _p(v), v.stride(0), hs(v_head_stride), _p(o), o.stride(0), hs(o_head_stride), q.shape[0],
                  k.shape[0], heads, head_dim, float(scale), _p(run_flag), int(run_if), _stream())
     return o
@@ -102,46 +153,46 @@ def gemv(w, x, out, bias=None, add=None, in_silu=False, t=None):
     """out[f32] = w @ in(x) + bias + add  (x f32, or timestep features of device scalar t)."""
     _need(w, BF16, "gemv.w")
     n, k = w.shape
-    _native.call("aqb_gemv", _p(w), _p(x), _p(t), _p(bias), _p(add), _p(out), n, k, int(bool(in_silu)), _stream())
+    _run("gemv", 2 * n * k, "aqb_gemv", _p(w), _p(x), _p(t), _p(bias), _p(add), _p(out), n, k, int(bool(in_silu)), _stream())
     return out
 
 
 def add_bcast(out, a, b):
-    _native.call("aqb_add_bcast", _p(out), _p(a), a.numel(), _p(b), b.numel(), _stream())
+    _run("small", 12 * b.numel(), "aqb_add_bcast", _p(out), _p(a), a.numel(), _p(b), b.numel(), _stream())
     return out
 
 
 def rel_l1_reduce(partials, rows, sums):
-    _native.call("aqb_rel_l1_reduce", _p(partials), rows, _p(sums), _stream())
+    _run("small", 8 * rows, "aqb_rel_l1_reduce", _p(partials), rows, _p(sums), _stream())
 
 
 def cache_decide(sums, state, threshold, warmup, total_steps, force_last, flags_out, rel_out):
-    _native.call("aqb_cache_decide", _p(sums), _p(state), float(threshold), int(warmup), int(total_steps),
+    _run("small", 0, "aqb_cache_decide", _p(sums), _p(state), float(threshold), int(warmup), int(total_steps),
                  int(bool(force_last)), _p(flags_out), _p(rel_out), _stream())
 
 
 def cache_offset(x, off, mode, run_flag=None, run_if=1):
     rows, hidden = off.shape
-    _native.call("aqb_cache_offset", _p(x), x.stride(0), _p(off), rows, hidden, int(mode), _p(run_flag),
+    _run("cache_offset", (8 if mode == 0 else 12) * rows * hidden, "aqb_cache_offset", _p(x), x.stride(0), _p(off), rows, hidden, int(mode), _p(run_flag),
                  int(run_if), _stream())
 
 
 def step_scalars(ts, dts, idx, cur, advance=False):
-    _native.call("aqb_step_scalars", _p(ts), _p(dts), _p(idx), _p(cur), int(bool(advance)), _stream())
+    _run("small", 0, "aqb_step_scalars", _p(ts), _p(dts), _p(idx), _p(cur), int(bool(advance)), _stream())
 
 
 def patchify(lat, tok, tok_bf16, grid, patch):
     C = lat.shape[0]
-    _native.call("aqb_patchify", _p(lat), _p(tok), _p(tok_bf16), C, grid[0], grid[1], grid[2], patch[0], patch[1],
+    _run("layout", 10 * lat.numel(), "aqb_patchify", _p(lat), _p(tok), _p(tok_bf16), C, grid[0], grid[1], grid[2], patch[0], patch[1],
                  patch[2], _stream())
 
 
 def unpatchify(tok, lat, grid, patch):
     C = lat.shape[0]
-    _native.call("aqb_unpatchify", _p(tok), _p(lat), C, grid[0], grid[1], grid[2], patch[0], patch[1], patch[2],
+    _run("layout", 8 * lat.numel(), "aqb_unpatchify", _p(tok), _p(lat), C, grid[0], grid[1], grid[2], patch[0], patch[1], patch[2],
                  _stream())
 
 
 def heads_to_seq(src, rows, P, width, dst, run_flag=None, run_if=1):
-    _native.call("aqb_heads_to_seq", _p(src), rows, P, width, _p(dst), dst.stride(0), _p(run_flag), int(run_if),
+    _run("layout", 4 * rows * P * width, "aqb_heads_to_seq", _p(src), rows, P, width, _p(dst), dst.stride(0), _p(run_flag), int(run_if),
                  _stream())

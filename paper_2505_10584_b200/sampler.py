@@ -39,7 +39,7 @@ class _Graphs:
         self.g = {}
 
     def run(self, model, mode, use_cache):
-        key = (mode, use_cache)
+        key = (id(model), model.generation, mode, use_cache, id(model.policy))
         if key not in self.g:
             # warm the kernels' one-time attribute setup outside capture
             s = torch.cuda.Stream()
