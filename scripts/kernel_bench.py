@@ -1,0 +1,139 @@
+#!/usr/bin/env python
+"""Per-kernel microbenchmarks at BASELINE shapes (CUDA events, warm, L2-flushed).
+
+    python scripts/kernel_bench.py [--only gemm|attn|norm] [--ncu] [--attn-sweep]
+
+--ncu: run each kernel a few times without timing loops (for ncu -k regex:...).
+--attn-sweep: BASELINE config 5 — joint-attention seq 4k..128k, head_dim 128,
+  24 heads (per GPU: 24/P heads at full sequence after the Ulysses all-to-all).
+"""
+
+import argparse
+import json
+import os
+import sys
+
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+from paper_2505_10584_b200 import ops  # noqa: E402
+
+dev = "cuda"
+FLUSH = None
+
+
+def flush_l2():
+    global FLUSH
+    if FLUSH is None:
+        FLUSH = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    FLUSH.zero_()
+
+
+def timeit(fn, iters=10, flush=True):
+    for _ in range(3):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(iters):
+        if flush:
+            flush_l2()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    ts.sort()
+    return ts[len(ts) // 2]
+
+
+def gemm_case(m, n, k, epi="bf16", ncu=False):
+    a = torch.randn(m, k, device=dev).to(torch.bfloat16)
+    w = (torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)
+    b = torch.randn(n, device=dev)
+    if epi in ("bf16", "gelu"):
+        out = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+    else:
+        out = torch.zeros(m, n, device=dev)
+    g = torch.randn(n, device=dev)
+    fn = lambda: ops.gemm(a, w, out, bias=b, gate=g if epi == "gate_res" else None, epilogue=epi)  # noqa: E731
+    if ncu:
+        fn()
+        return None
+    ms = timeit(fn)
+    return {"kernel": "gemm", "m": m, "n": n, "k": k, "epi": epi, "ms": ms, "tflops": 2 * m * n * k / ms / 1e9}
+
+
+def attn_case(sq, skv, heads, d=128, ncu=False, packed=True):
+    qkv = torch.randn(max(sq, skv), 3 * heads * d, device=dev).to(torch.bfloat16)
+    o = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
+    H = heads * d
+    fn = lambda: ops.attention(qkv[:sq], qkv[:skv, H:], qkv[:skv, 2 * H:], o, heads, d)  # noqa: E731
+    if ncu:
+        fn()
+        return None
+    ms = timeit(fn, iters=5)
+    fl = 4.0 * sq * skv * d * heads
+    return {"kernel": "attention", "sq": sq, "skv": skv, "heads": heads, "d": d, "ms": ms, "tflops": fl / ms / 1e9}
+
+
+def norm_case(rows, hidden, ncu=False):
+    x = torch.randn(rows, hidden, device=dev)
+    y = torch.empty(rows, hidden, device=dev, dtype=torch.bfloat16)
+    sh = torch.randn(hidden, device=dev)
+    sc = torch.randn(hidden, device=dev)
+    fn = lambda: ops.norm_modulate(x, sh, sc, y)  # noqa: E731
+    if ncu:
+        fn()
+        return None
+    ms = timeit(fn)
+    return {"kernel": "norm_modulate", "rows": rows, "hidden": hidden, "ms": ms, "gbs": rows * hidden * 6 / ms / 1e6}
+
+
+def qk_case(rows, heads, d=128, ncu=False):
+    qkv = torch.randn(rows, 3 * heads * d, device=dev).to(torch.bfloat16)
+    qw = torch.ones(d, device=dev)
+    cos = torch.randn(rows, d // 2, device=dev)
+    sin = torch.randn(rows, d // 2, device=dev)
+    fn = lambda: ops.qk_norm_rope(qkv, heads, d, qw, qw, 1e-6, cos, sin, 0, rows)  # noqa: E731
+    if ncu:
+        fn()
+        return None
+    ms = timeit(fn)
+    return {"kernel": "qk_norm_rope", "rows": rows, "heads": heads, "ms": ms,
+            "gbs": rows * 3 * heads * d * 2 * 2 / ms / 1e6}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="all")
+    ap.add_argument("--ncu", action="store_true")
+    ap.add_argument("--attn-sweep", action="store_true")
+    args = ap.parse_args()
+    res = []
+    S, H = 7800, 2048
+    if args.only in ("all", "gemm"):
+        for (m, n, k, e) in [(S, 3 * H, H, "bf16"), (S, H, H, "gate_res"), (S, 4 * H, H, "gelu"), (S, H, 4 * H, "gate_res"),
+                             (14850 + 256, 3 * 3072, 3072, "bf16"), (8192, 8192, 8192, "bf16")]:
+            res.append(gemm_case(m, n, k, e, args.ncu))
+    if args.only in ("all", "attn"):
+        res.append(attn_case(S, S, 16, 128, args.ncu))
+        res.append(attn_case(S, 256, 16, 128, args.ncu))
+        if not args.ncu:
+            res.append(attn_case(118800 + 256, 118800 + 256, 3, 128))  # config 4 per rank at P=8
+    if args.only in ("all", "norm"):
+        res.append(norm_case(S, H, args.ncu))
+        res.append(qk_case(S, 16, 128, args.ncu))
+    if args.attn_sweep:
+        for s in (4096, 8192, 16384, 32768, 65536, 131072):
+            for P in (1, 2, 4, 8):
+                if s >= 65536 and P == 1:
+                    continue
+                res.append(attn_case(s, s, 24 // P, 128))
+    for r in res:
+        if r:
+            print(json.dumps(r), flush=True)
+
+
+if __name__ == "__main__":
+    main()
