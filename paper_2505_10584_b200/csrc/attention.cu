@@ -10,12 +10,16 @@
 //   warp 0      TMA producer: Q0, Q1 once; K_j, V_j through an NS-deep ring.
 //   warp 1      MMA issuer (one thread):  S_t = Q_t K_j^T  (SS, M=128 N=128)
 //               O_t += P_t V_j  (P from smem K-major, V MN-major, N=D).
-//   warps 2-5   softmax of tile 0, warps 6-9 softmax of tile 1: thread = query
-//               row (TMEM lane).  Online softmax in the exp2 domain with
-//               lazy rescaling (only when the running max grows by > 8, so
-//               O in TMEM is rarely touched); P written to smem in the
-//               128B-swizzled K-major layout the MMA reads; final 1/l
-//               normalisation and bf16 store from the same warps.
+//   warps 4-7   softmax of tile 0, warps 8-11 softmax of tile 1: thread = query
+//               row (TMEM lane), 224 registers each (setmaxnreg).  Online
+//               softmax in the exp2 domain: scale folded into one packed
+//               FFMA2 per pair, 3/8 of the exponentials evaluated by a
+//               degree-3 polynomial on the FMA pipe (the rest on MUFU) so
+//               neither pipe caps the tensor core; lazy rescaling (only when
+//               the running max grows by > 8, so O in TMEM is rarely
+//               touched); P written with st.shared.v4 in the 128B-swizzled
+//               K-major layout the MMA reads; final 1/l normalisation and
+//               bf16 store from the same warps.
 // TMEM: S0 | S1 | O0 | O1  (128 + 128 + D + D columns).
 #include <cmath>
 
@@ -27,7 +31,10 @@ namespace attn {
 
 constexpr int BQ = 128;   // rows per Q tile (MMA M)
 constexpr int BKV = 128;  // keys per KV tile (MMA N of QK^T, K of PV)
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;    // 3 warpgroups: control | softmax tile 0 | softmax tile 1
+constexpr uint32_t kCtrlRegs = 56;     // setmaxnreg budgets: 56 + 2 * 224 <= 512 per SMSP
+constexpr uint32_t kSoftmaxRegs = 224;
+constexpr uint32_t kPolyMask = 0x52;   // pairs (i & 7) in {1,4,6}: exp2 by polynomial (3/8 off the MUFU)
 
 template <int D>
 struct Cfg {
@@ -101,6 +108,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (warp == 0) {
     // ------------------------------------------------------------ producer
+    setmaxnreg_dec<kCtrlRegs>();
     if (lane == 0) {
       mbar_arrive_expect_tx(q_full, 2 * C::kQBytes);
       for (int t = 0; t < 2; ++t)
@@ -119,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    setmaxnreg_dec<kCtrlRegs>();
     if (lane == 0) {
       constexpr uint32_t kIdescS = idesc_bf16(BQ, BKV, 0, 0);  // Q, K both K-major
       constexpr uint32_t kIdescO = idesc_bf16(BQ, D, 0, 1);    // P K-major, V MN-major
@@ -174,80 +183,104 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     }
-  } else {
+  } else if (warp >= 4) {
     // ------------------------------------------------------------ softmax
-    const int t = (warp - 2) / 4;             // Q tile of this warpgroup
+    setmaxnreg_inc<kSoftmaxRegs>();
+    const int t = (warp - 4) / 4;             // Q tile of this warpgroup
     const uint32_t quad = warp & 3;           // TMEM lane quadrant
     const int r = quad * 32 + lane;           // row within the tile
     const uint32_t lane_base = (quad * 32) << 16;
     const uint32_t s_tmem = tmem + lane_base + t * 128;
     const uint32_t o_tmem = tmem + lane_base + 256 + t * D;
-    uint8_t* prow = sP + t * C::kPBytes + r * 128;
+    const uint32_t prow = smem_u32(sP + t * C::kPBytes + r * 128);
     const uint32_t sw = r & 7;
-    float m_run = -INFINITY, l_run = 0.f;
+    const float c = p.scale_log2;
+    const uint64_t c2 = f2pack(c, c);
+    const uint64_t kM = f2pack(12582912.f, 12582912.f);  // 1.5 * 2^23: round-to-nearest
+    const uint64_t kC0 = f2pack(0.99992806f, 0.99992806f), kC1 = f2pack(0.69326103f, 0.69326103f);
+    const uint64_t kC2 = f2pack(0.24261117f, 0.24261117f), kC3 = f2pack(0.05517162f, 0.05517162f);
+    float m_run = -INFINITY, l_run = 0.f;     // m_run in raw score units
 
     for (int j = 0; j < nkv; ++j) {
       mbar_wait(s_full + t, j & 1);
       tc_fence_after();
-      float s[BKV];
-      {
-        uint32_t u[32];
-#pragma unroll
-        for (int c = 0; c < BKV / 32; ++c) {
-          tmem_ld32(s_tmem + c * 32, u);
-          tmem_wait_ld();
-#pragma unroll
-          for (int i = 0; i < 32; ++i) s[c * 32 + i] = __uint_as_float(u[i]) * p.scale_log2;
-        }
-      }
+      uint32_t sr[BKV];
+      tmem_ld64(s_tmem, sr);
+      tmem_ld64(s_tmem + 64, sr + 64);
+      tmem_wait_ld();
       const int kv_valid = p.seq_kv - j * BKV;
       if (kv_valid < BKV) {
 #pragma unroll
         for (int i = 0; i < BKV; ++i)
-          if (i >= kv_valid) s[i] = -INFINITY;
+          if (i >= kv_valid) sr[i] = 0xff800000u;  // -inf
       }
-      float mx = s[0];
+      float mx = __uint_as_float(sr[0]);
 #pragma unroll
-      for (int i = 1; i < BKV; ++i) mx = fmaxf(mx, s[i]);
+      for (int i = 1; i + 1 < BKV; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
+      mx = fmaxf(mx, __uint_as_float(sr[BKV - 1]));
       // PV_{j-1} must be done before O is rescaled or P_t overwritten.
       if (j > 0) {
         mbar_wait(o_ready + t, (j - 1) & 1);
         tc_fence_after();
       }
-      const bool need = mx > m_run + 8.f;
+      // lazy rescale: only when the running max grows by more than 2^8 in exp2 units
+      const bool need = (mx - m_run) * c > 8.f;
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? mx : m_run;
-        const float alpha = need ? ex2(m_run - m_new) : 1.f;
+        const float alpha = need ? ex2((m_run - m_new) * c) : 1.f;
         if (j > 0) {
 #pragma unroll 1
-          for (int c = 0; c < D / 32; ++c) {
+          for (int cc = 0; cc < D / 32; ++cc) {
             uint32_t u[32];
-            tmem_ld32(o_tmem + c * 32, u);
+            tmem_ld32(o_tmem + cc * 32, u);
             tmem_wait_ld();
 #pragma unroll
             for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-            tmem_st32(o_tmem + c * 32, u);
+            tmem_st32(o_tmem + cc * 32, u);
           }
           tmem_wait_st();
         }
         l_run *= alpha;
         m_run = m_new;
       }
-      float sum = 0.f;
+      const float nm = -m_run * c;
+      const uint64_t nm2 = f2pack(nm, nm);
+      uint64_t acc2 = f2pack(0.f, 0.f);
 #pragma unroll
       for (int kc = 0; kc < BKV / 8; ++kc) {  // 16-byte chunks of the P row
-        float e[8];
+        uint32_t pk[4];
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          e[i] = ex2(s[kc * 8 + i] - m_run);
-          sum += e[i];
+        for (int q = 0; q < 4; ++q) {
+          const int pi = kc * 4 + q;
+          const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * pi]), __uint_as_float(sr[2 * pi + 1])), c2, nm2);
+          float x0, x1, p0, p1;
+          f2unpack(x2, x0, x1);
+          if ((kPolyMask >> (pi & 7)) & 1) {
+            // exp2 on the FMA pipe: 2^x = 2^round(x) * poly(x - round(x)), |rel err| < 8e-5
+            const uint64_t xc = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+            const uint64_t tt = fadd2(xc, kM);
+            const uint64_t fr = fsub2(xc, fsub2(tt, kM));
+            uint64_t pp = ffma2(fr, kC3, kC2);
+            pp = ffma2(pp, fr, kC1);
+            pp = ffma2(pp, fr, kC0);
+            float q0, q1, t0, t1;
+            f2unpack(pp, q0, q1);
+            f2unpack(tt, t0, t1);
+            p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+            p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+          } else {
+            p0 = ex2(x0);
+            p1 = ex2(x1);
+          }
+          acc2 = fadd2(acc2, f2pack(p0, p1));
+          pk[q] = pack_bf16(p0, p1);
         }
-        const uint4 pk = make_uint4(pack_bf16(e[0], e[1]), pack_bf16(e[2], e[3]), pack_bf16(e[4], e[5]),
-                                    pack_bf16(e[6], e[7]));
-        const int box = kc >> 3, c = kc & 7;
-        *reinterpret_cast<uint4*>(prow + box * (BQ * 128) + ((c ^ sw) << 4)) = pk;
+        const int box = kc >> 3, cch = kc & 7;
+        st_shared_v4(prow + box * (BQ * 128) + ((cch ^ sw) << 4), pk[0], pk[1], pk[2], pk[3]);
       }
-      l_run += sum;
+      float a0, a1;
+      f2unpack(acc2, a0, a1);
+      l_run += a0 + a1;
       fence_proxy_async_smem();  // generic-proxy P stores -> visible to the tensor core
       tc_fence_before();
       mbar_arrive(p_full + t);
@@ -259,21 +292,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
     __nv_bfloat16* orow = p.o + static_cast<int64_t>(head) * p.o_head_stride + static_cast<int64_t>(row) * p.ldo;
 #pragma unroll 1
-    for (int c = 0; c < D / 32; ++c) {
+    for (int cc = 0; cc < D / 32; ++cc) {
       uint32_t u[32];
-      tmem_ld32(o_tmem + c * 32, u);
+      tmem_ld32(o_tmem + cc * 32, u);
       tmem_wait_ld();
-      if (row < p.seq_q && c * 32 < p.head_dim) {
+      if (row < p.seq_q && cc * 32 < p.head_dim) {
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
           const uint4 pk = make_uint4(pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
                                       pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
                                       pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
                                       pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
-          *reinterpret_cast<uint4*>(orow + c * 32 + 8 * g) = pk;
+          *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = pk;
         }
       }
     }
+  } else {
+    setmaxnreg_dec<kCtrlRegs>();
   }
   tc_fence_before();
   __syncthreads();
