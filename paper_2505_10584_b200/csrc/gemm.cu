@@ -6,17 +6,29 @@
 // GeLU and Gate fused into the epilogue, plus the
 // flow-matching Euler update for the final layer.
 //
-// Structure (one CTA per SM, persistent over output tiles):
-//   warp 0      TMA producer: A[128 x 64] + W[BN x 64] per k-block into a
-//               STAGES-deep ring (128B swizzle), mbarrier full/empty.
-//   warp 1      MMA issuer: one elected thread issues tcgen05.mma (M=128,
-//               N=BN, K=16) into one of two TMEM accumulators (2 x BN columns),
-//               tcgen05.commit frees smem stages / signals the epilogue.
-//   warp 2      TMEM allocator.
-//   warps 4-7   epilogue: tcgen05.ld 32 columns at a time (thread = row),
-//               bias / GeLU / gate*residual / Euler, vectorised global stores;
-//               overlaps the MMA of the next tile (double-buffered TMEM).
+// Two kernels share one epilogue:
+//  * gemm_kernel   1 CTA per 128 x BN tile (cta_group::1, UMMA M=128).
+//  * gemm2_kernel  a CTA pair (cluster of 2) per 256 x BN tile: each CTA loads
+//                  its 128 rows of A and BN/2 rows of W, the leader issues
+//                  cta_group::2 MMAs (M=256) that read both CTAs' smem and write
+//                  both CTAs' TMEM — half the W bytes per SM (L2->SM operand
+//                  bandwidth is what limits 1-CTA tiles).
+// Roles (both): warp 0 TMA producer (STAGES-deep 128B-swizzled ring, mbarrier
+// full/empty), warp 1 MMA issuer (single thread, TMEM double-buffered 2 x BN
+// columns so the epilogue of tile i overlaps the MMAs of tile i+1), warp 2 TMEM
+// allocator, warp 3 idle, warps 4-7 epilogue.
+//
+// Epilogue: per 128-byte-wide column chunk (32 fp32 / 64 bf16 columns), each
+// thread (= one TMEM lane = one row) pulls its accumulators with tcgen05.ld,
+// the residual chunk (gate*residual) arrives by TMA into a 128B-swizzled smem
+// buffer, the thread combines bias / GeLU / gate / residual in registers,
+// writes the result back to the swizzled buffer (conflict-free 16 B accesses),
+// and one thread TMA-stores the chunk.  All global traffic is TMA (coalesced);
+// the two smem buffers alternate so a chunk's store overlaps the next chunk.
+#include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "host.cuh"
 #include "ptx.cuh"
@@ -27,6 +39,7 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
 constexpr int kThreads = 256;
+constexpr int kEpiBuf = 128 * 128;  // one epilogue chunk: 128 rows x 128 B
 
 struct Params {
   int M, N, K;
@@ -52,95 +65,199 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int
   nb = r / gsz;
 }
 
-template <int BN, int STAGES>
-constexpr int smem_bytes() {
-  return STAGES * (BM + BN) * BK * 2 + 1024 /*align slack*/ + 256 /*barriers*/;
+__device__ __forceinline__ float4 ld_f4(const float* p) {
+  float4 r;
+  asm volatile("ld.global.v4.f32 {%0,%1,%2,%3}, [%4];" : "=f"(r.x), "=f"(r.y), "=f"(r.z), "=f"(r.w) : "l"(p));
+  return r;
+}
+__device__ __forceinline__ void st_f4(float* p, float4 v) {
+  asm volatile("st.global.v4.f32 [%0], {%1,%2,%3,%4};" ::"l"(p), "f"(v.x), "f"(v.y), "f"(v.z), "f"(v.w) : "memory");
 }
 
-template <int EPI>
-__device__ __forceinline__ void epilogue_chunk(const Params& p, int row, int col0, const uint32_t (&r)[32]) {
+// Euler epilogue of the (tiny, N = patch_dim) final layer: direct stores.
+__device__ __forceinline__ void euler_chunk(const Params& p, int row, int col0, const uint32_t (&r)[32]) {
   float v[32];
 #pragma unroll
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
   if (p.bias != nullptr) {
-    const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (col0 + 4 * i < p.N) {
-        float4 b = __ldg(b4 + i);
-        v[4 * i] += b.x, v[4 * i + 1] += b.y, v[4 * i + 2] += b.z, v[4 * i + 3] += b.w;
-      }
-    }
+    for (int i = 0; i < 32; ++i)
+      if (col0 + i < p.N) v[i] += __ldg(p.bias + col0 + i);
   }
   if (row >= p.M) return;
-  if constexpr (EPI == AQB_EPI_BF16 || EPI == AQB_EPI_GELU_BF16) {
-    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(p.out) + static_cast<int64_t>(row) * p.ldo + col0;
+  const float a = __ldg(p.alpha);
+  float* out = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo + col0;
+  __nv_bfloat16* aux = p.aux + static_cast<int64_t>(row) * p.ld_aux + col0;
+  float4 xs[8];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (col0 + 8 * i < p.N) {
-        float t[8];
+  for (int i = 0; i < 8; ++i) xs[i] = (col0 + 4 * i < p.N) ? ld_f4(out + 4 * i) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
-        for (int j = 0; j < 8; ++j) t[j] = (EPI == AQB_EPI_GELU_BF16) ? gelu_tanh(v[8 * i + j]) : v[8 * i + j];
-        uint4 pk = make_uint4(pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
-                              pack_bf16(t[6], t[7]));
-        *reinterpret_cast<uint4*>(out + 8 * i) = pk;
-      }
-    }
-  } else if constexpr (EPI == AQB_EPI_F32) {
-    float* out = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo + col0;
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-      if (col0 + 4 * i < p.N)
-        *reinterpret_cast<float4*>(out + 4 * i) = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
-  } else if constexpr (EPI == AQB_EPI_GATE_RES) {
-    float* out = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo + col0;
-    const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (col0 + 4 * i < p.N) {
-        float4 x = *reinterpret_cast<float4*>(out + 4 * i);
-        float4 g = p.gate ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
-        x.x += g.x * v[4 * i];
-        x.y += g.y * v[4 * i + 1];
-        x.z += g.z * v[4 * i + 2];
-        x.w += g.w * v[4 * i + 3];
-        *reinterpret_cast<float4*>(out + 4 * i) = x;
-      }
-    }
-  } else if constexpr (EPI == AQB_EPI_EULER) {
-    const float a = __ldg(p.alpha);
-    float* out = reinterpret_cast<float*>(p.out) + static_cast<int64_t>(row) * p.ldo + col0;
-    __nv_bfloat16* aux = p.aux + static_cast<int64_t>(row) * p.ld_aux + col0;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (col0 + 8 * i < p.N) {
-        float4 x0 = *reinterpret_cast<float4*>(out + 8 * i);
-        float4 x1 = *reinterpret_cast<float4*>(out + 8 * i + 4);
-        x0.x += a * v[8 * i + 0], x0.y += a * v[8 * i + 1], x0.z += a * v[8 * i + 2], x0.w += a * v[8 * i + 3];
-        x1.x += a * v[8 * i + 4], x1.y += a * v[8 * i + 5], x1.z += a * v[8 * i + 6], x1.w += a * v[8 * i + 7];
-        *reinterpret_cast<float4*>(out + 8 * i) = x0;
-        *reinterpret_cast<float4*>(out + 8 * i + 4) = x1;
-        if (p.aux)
-          *reinterpret_cast<uint4*>(aux + 8 * i) = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w),
-                                                              pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
-      }
+  for (int i = 0; i < 4; ++i) {
+    if (col0 + 8 * i < p.N) {
+      float4 x0 = xs[2 * i], x1 = xs[2 * i + 1];
+      x0.x += a * v[8 * i + 0], x0.y += a * v[8 * i + 1], x0.z += a * v[8 * i + 2], x0.w += a * v[8 * i + 3];
+      x1.x += a * v[8 * i + 4], x1.y += a * v[8 * i + 5], x1.z += a * v[8 * i + 6], x1.w += a * v[8 * i + 7];
+      st_f4(out + 8 * i, x0);
+      st_f4(out + 8 * i + 4, x1);
+      if (p.aux)
+        *reinterpret_cast<uint4*>(aux + 8 * i) = make_uint4(pack_bf16(x0.x, x0.y), pack_bf16(x0.z, x0.w),
+                                                            pack_bf16(x1.x, x1.y), pack_bf16(x1.z, x1.w));
     }
   }
 }
 
+// Per-CTA epilogue state (warps 4-7 only).
+struct EpiState {
+  uint8_t* buf;      // kEpiBufs(EPI) x kEpiBuf, 1024-aligned
+  uint64_t* bar;     // one mbarrier per buffer (residual TMA loads)
+  uint32_t chunk;    // chunks processed by this CTA (buffer / phase bookkeeping)
+};
+
+// gate*residual keeps three buffers so the residual of chunk c+1 streams in
+// while chunk c is combined; the store-only epilogues need two.
+template <int EPI>
+constexpr int epi_bufs() { return EPI == AQB_EPI_GATE_RES ? 3 : 2; }
+
+template <int EPI>
+constexpr int epi_cols() { return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES) ? 32 : 64; }
+
+// Residual prefetch for the first chunk of a tile, issued before the
+// accumulator wait so its latency hides behind the tile's MMAs.
+template <int EPI>
+__device__ __forceinline__ void epilogue_prologue(const Params& p, const CUtensorMap* tmo, EpiState& es, int row0,
+                                                  int col_base, bool leader_thread) {
+  if constexpr (EPI == AQB_EPI_GATE_RES) {
+    if (leader_thread && col_base < p.N) {
+      const uint32_t b = es.chunk % 3;
+      bulk_wait_read<2>();  // buffer b was last stored 3 chunks ago
+      mbar_arrive_expect_tx(es.bar + b, kEpiBuf);
+      tma_load_2d(es.buf + b * kEpiBuf, tmo, es.bar + b, col_base, row0, kEvictFirst);
+    }
+  }
+}
+
+// One accumulator tile (this CTA's 128 rows x BN columns starting at col_base).
+template <int EPI, int BN>
+__device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmo, EpiState& es, uint32_t tacc,
+                                              int row0, int col_base, uint32_t q, uint32_t lane) {
+  const int r = q * 32 + lane;           // row within the CTA tile (= TMEM lane)
+  const uint32_t lane_off = (q * 32) << 16;
+  const bool leader_thread = (q == 0 && lane == 0);
+  if constexpr (EPI == AQB_EPI_EULER) {
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      if (col_base + c >= p.N) break;
+      uint32_t u[32];
+      tmem_ld32(tacc + c + lane_off, u);
+      tmem_wait_ld();
+      euler_chunk(p, row0 + r, col_base + c, u);
+    }
+    return;
+  } else {
+    constexpr int NB = epi_bufs<EPI>();
+    constexpr int CW = epi_cols<EPI>();  // columns per 128-byte chunk
+#pragma unroll 1
+    for (int c = 0; c < BN; c += CW) {
+      const int col0 = col_base + c;
+      if (col0 >= p.N) break;  // uniform over the 128 epilogue threads
+      const uint32_t b = es.chunk % NB;
+      uint8_t* buf = es.buf + b * kEpiBuf;
+      if constexpr (EPI == AQB_EPI_GATE_RES) {
+        // this chunk's residual was requested one chunk (or one tile) ago; request the next one
+        if (leader_thread && c + CW < BN && col0 + CW < p.N) {
+          const uint32_t bn = (es.chunk + 1) % NB;
+          bulk_wait_read<1>();  // buffer bn was last stored two chunks ago
+          mbar_arrive_expect_tx(es.bar + bn, kEpiBuf);
+          tma_load_2d(es.buf + bn * kEpiBuf, tmo, es.bar + bn, col0 + CW, row0, kEvictFirst);
+        }
+      } else {
+        // buffer b was last read by the TMA store issued NB chunks ago
+        if (leader_thread) bulk_wait_read<NB - 1>();
+        named_bar_sync(1, 128);
+      }
+      float v[CW];
+      {
+        uint32_t u[32];
+#pragma unroll
+        for (int h = 0; h < CW / 32; ++h) {
+          tmem_ld32(tacc + c + 32 * h + lane_off, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[32 * h + i] = __uint_as_float(u[i]);
+        }
+      }
+      if (p.bias != nullptr) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
+#pragma unroll
+        for (int i = 0; i < CW / 4; ++i) {
+          if (col0 + 4 * i < p.N) {
+            const float4 bb = __ldg(b4 + i);
+            v[4 * i] += bb.x, v[4 * i + 1] += bb.y, v[4 * i + 2] += bb.z, v[4 * i + 3] += bb.w;
+          }
+        }
+      }
+      const uint32_t rowaddr = smem_u32(buf) + r * 128;
+      const uint32_t sw = r & 7;
+      if constexpr (EPI == AQB_EPI_GATE_RES) {
+        mbar_wait(es.bar + b, (es.chunk / NB) & 1);
+        const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const uint32_t a = rowaddr + ((i ^ sw) << 4);
+          const uint4 xr = lds128(a);
+          const float4 g = (p.gate && col0 + 4 * i < p.N) ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+          st_shared_v4(a, __float_as_uint(__uint_as_float(xr.x) + g.x * v[4 * i]),
+                       __float_as_uint(__uint_as_float(xr.y) + g.y * v[4 * i + 1]),
+                       __float_as_uint(__uint_as_float(xr.z) + g.z * v[4 * i + 2]),
+                       __float_as_uint(__uint_as_float(xr.w) + g.w * v[4 * i + 3]));
+        }
+      } else if constexpr (EPI == AQB_EPI_F32) {
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(v[4 * i]), __float_as_uint(v[4 * i + 1]),
+                       __float_as_uint(v[4 * i + 2]), __float_as_uint(v[4 * i + 3]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float t[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) t[j] = (EPI == AQB_EPI_GELU_BF16) ? gelu_tanh(v[8 * i + j]) : v[8 * i + j];
+          st_shared_v4(rowaddr + ((i ^ sw) << 4), pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
+                       pack_bf16(t[6], t[7]));
+        }
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1, 128);
+      if (leader_thread) {
+        tma_store_2d(tmo, buf, col0, row0);  // clips rows >= M and columns >= N
+        bulk_commit();
+      }
+      ++es.chunk;
+    }
+  }
+}
+
+template <int BN, int STAGES, bool PAIR, int EPI>
+constexpr int smem_bytes() {
+  return STAGES * (BM + (PAIR ? BN / 2 : BN)) * BK * 2 + epi_bufs<EPI>() * kEpiBuf + 1024 /*align*/ + 256 /*bars*/;
+}
+
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
-    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b, Params p) {
+    gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                const __grid_constant__ CUtensorMap tma_o, Params p) {
   if (!gate_open(p.run_flag, p.run_if)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(base);
   __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(base + STAGES * BM * BK * 2);
-  uint64_t* full = reinterpret_cast<uint64_t*>(base + STAGES * (BM + BN) * BK * 2);
+  uint8_t* ebuf = base + STAGES * (BM + BN) * BK * 2;
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* ebar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 3);
 
   constexpr uint32_t kTmemCols = 2 * BN;
   const uint32_t warp = warp_idx(), lane = lane_idx();
@@ -148,6 +265,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma_a);
     tma_prefetch_desc(&tma_b);
+    tma_prefetch_desc(&tma_o);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
@@ -156,6 +274,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 4);
     }
+    for (int b = 0; b < 3; ++b) mbar_init(ebar + b, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -198,11 +317,9 @@ __global__ void __launch_bounds__(kThreads, 1)
           const uint32_t a0 = smem_u32(sa + stage * BM * BK);
           const uint32_t b0 = smem_u32(sb + stage * BN * BK);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
+          for (int k = 0; k < BK / 16; ++k)
             // K-major SW128: +32 B per 16-element K step inside the 128 B swizzle row.
-            umma_bf16_ss(d, smem_desc(a0 + 32 * k, 0, 1024), smem_desc(b0 + 32 * k, 0, 1024), kIdesc,
-                         (kb | k) != 0);
-          }
+            umma_bf16_ss(d, smem_desc(a0 + 32 * k, 0, 1024), smem_desc(b0 + 32 * k, 0, 1024), kIdesc, (kb | k) != 0);
           umma_commit(empty + stage);
           if (++stage == STAGES) stage = 0, phase ^= 1;
         }
@@ -213,29 +330,23 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
+    EpiState es{ebuf, ebar, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
+      epilogue_prologue<EPI>(p, &tma_o, es, mb * BM, nb * BN, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      const int row = mb * BM + q * 32 + lane;
-#pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
-        const int col0 = nb * BN + c;
-        if (col0 >= p.N) break;  // warp-uniform
-        uint32_t r[32];
-        tmem_ld32(tmem + acc * BN + c + ((q * 32) << 16), r);
-        tmem_wait_ld();
-        epilogue_chunk<EPI>(p, row, col0, r);
-      }
+      epilogue_tile<EPI, BN>(p, &tma_o, es, tmem + acc * BN, mb * BM, nb * BN, q, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
+    if (q == 0 && lane == 0) bulk_wait<0>();
   }
   tc_fence_before();
   __syncthreads();
@@ -246,43 +357,203 @@ __global__ void __launch_bounds__(kThreads, 1)
 }
 
 template <int BN, int STAGES, int EPI>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t stream) {
-  constexpr int smem = smem_bytes<BN, STAGES>();
-  static bool configured = false;  // per instantiation; attribute is per-function
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
+    gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
+                 const __grid_constant__ CUtensorMap tma_o, Params p) {
+  if (!gate_open(p.run_flag, p.run_if)) return;
+  constexpr int BNH = BN / 2;  // W rows per CTA
+  constexpr int kABytes = BM * BK * 2, kBBytes = BNH * BK * 2;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sa = base;
+  uint8_t* sb = base + STAGES * kABytes;
+  uint8_t* ebuf = base + STAGES * (kABytes + kBBytes);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* ebar = tempty + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 3);
+
+  constexpr uint32_t kTmemCols = 2 * BN;
+  const uint32_t warp = warp_idx(), lane = lane_idx();
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tma_a);
+    tma_prefetch_desc(&tma_b);
+    tma_prefetch_desc(&tma_o);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(full + s, 2);   // leader's expect_tx arrive + the peer's remote arrive
+      mbar_init(empty + s, 1);  // multicast MMA commit
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(tfull + a, 1);   // multicast MMA commit
+      mbar_init(tempty + a, 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
+    }
+    for (int b = 0; b < 3; ++b) mbar_init(ebar + b, 1);
+    fence_barrier_init();
+  }
+  cluster_sync();
+  if (warp == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
+  tc_fence_before();
+  cluster_sync();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int nk = (p.K + BK - 1) / BK;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+        int mb, nb;
+        tile_coords(p, t, mb, nb);
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(empty + stage, phase ^ 1);
+          tma_load_2d_pair(sa + stage * kABytes, &tma_a, full + stage, kb * BK, mb * (2 * BM) + rank * BM);
+          tma_load_2d_pair(sb + stage * kBBytes, &tma_b, full + stage, kb * BK, nb * BN + rank * BNH);
+          if (leader)
+            mbar_arrive_expect_tx(full + stage, 2 * (kABytes + kBBytes));
+          else
+            mbar_arrive_cluster(full + stage, 0);
+          if (++stage == STAGES) stage = 0, phase ^= 1;
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader && lane == 0) {
+      constexpr uint32_t kIdesc = idesc_bf16(2 * BM, BN, 0, 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+        mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t d = tmem + acc * BN;
+        for (int kb = 0; kb < nk; ++kb) {
+          mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const uint32_t a0 = smem_u32(sa + stage * kABytes);
+          const uint32_t b0 = smem_u32(sb + stage * kBBytes);
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k)
+            umma_bf16_pair(d, smem_desc(a0 + 32 * k, 0, 1024), smem_desc(b0 + 32 * k, 0, 1024), kIdesc, (kb | k) != 0);
+          umma_commit_pair(empty + stage);
+          if (++stage == STAGES) stage = 0, phase ^= 1;
+        }
+        umma_commit_pair(tfull + acc);
+        acc ^= 1;
+        if (acc == 0) acc_phase ^= 1;
+      }
+    }
+  } else if (warp >= 4) {
+    const uint32_t q = warp & 3;
+    EpiState es{ebuf, ebar, 0};
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = cluster; t < p.num_tiles; t += nclusters) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      epilogue_prologue<EPI>(p, &tma_o, es, mb * (2 * BM) + rank * BM, nb * BN, q == 0 && lane == 0);
+      mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      epilogue_tile<EPI, BN>(p, &tma_o, es, tmem + acc * BN, mb * (2 * BM) + rank * BM, nb * BN, q, lane);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) {
+        if (leader)
+          mbar_arrive(tempty + acc);
+        else
+          mbar_arrive_cluster(tempty + acc, 0);
+      }
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
+    }
+    if (q == 0 && lane == 0) bulk_wait<0>();
+  }
+  tc_fence_before();
+  cluster_sync();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc_pair(tmem, kTmemCols);
+  }
+}
+
+template <int BN, int STAGES, int EPI, bool PAIR>
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const Params& p, cudaStream_t stream) {
+  constexpr int smem = smem_bytes<BN, STAGES, PAIR, EPI>();
+  static_assert(smem <= 232448, "shared memory budget");
+  auto kern = PAIR ? gemm2_kernel<BN, STAGES, EPI> : gemm_kernel<BN, STAGES, EPI>;
+  static bool configured = false;  // per instantiation; the attribute is per function
   if (!configured) {
-    AQB_CUDA_TRY(cudaFuncSetAttribute(gemm_kernel<BN, STAGES, EPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    AQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  const int grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
-  gemm_kernel<BN, STAGES, EPI><<<grid, kThreads, smem, stream>>>(ta, tb, p);
+  int grid;
+  if (PAIR) {
+    const int pairs = sm_count() / 2;
+    grid = 2 * (p.num_tiles < pairs ? p.num_tiles : pairs);
+  } else {
+    grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
+  }
+  kern<<<grid, kThreads, smem, stream>>>(ta, tb, to, p);
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
 
-template <int BN, int STAGES>
-int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const Params& p, cudaStream_t s) {
+template <int BN, int STAGES, bool PAIR>
+int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const Params& p,
+                 cudaStream_t s) {
+  // one pipeline stage makes room for the third gate*residual buffer
+  constexpr int kResStages = STAGES - ((PAIR ? BM + BN / 2 : BM + BN) * BK * 2 >= kEpiBuf * 2 ? 1 : 1);
   switch (epi) {
-    case AQB_EPI_BF16: return launch<BN, STAGES, AQB_EPI_BF16>(ta, tb, p, s);
-    case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16>(ta, tb, p, s);
-    case AQB_EPI_GATE_RES: return launch<BN, STAGES, AQB_EPI_GATE_RES>(ta, tb, p, s);
-    case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32>(ta, tb, p, s);
-    case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER>(ta, tb, p, s);
+    case AQB_EPI_BF16: return launch<BN, STAGES, AQB_EPI_BF16, PAIR>(ta, tb, to, p, s);
+    case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16, PAIR>(ta, tb, to, p, s);
+    case AQB_EPI_GATE_RES: return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, p, s);
+    case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32, PAIR>(ta, tb, to, p, s);
+    case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER, PAIR>(ta, tb, to, p, s);
   }
   return set_error(AQB_EINVAL, "unknown epilogue %d", epi);
 }
 
-// Pick the N tile: 256 (lower smem-operand traffic per MMA) unless it leaves
-// the last wave badly under-filled relative to 128.
-static int pick_bn(int64_t m, int64_t n) {
-  if (n <= 128) return 128;
-  const int sms = sm_count();
-  auto eff = [&](int bn) {
-    const double tiles = double((m + BM - 1) / BM) * double((n + bn - 1) / bn);
-    const double waves = tiles / sms;
-    const double used = tiles * bn;  // useful-ish work units
-    return used / (std::ceil(waves) * sms * bn) * (bn == 256 ? 1.0 : 0.9);  // 128-wide tiles pay smem bw
-  };
-  return eff(256) >= eff(128) ? 256 : 128;
+// Variant choice.  Cost model: waves of tiles x per-tile time, where the
+// per-tile time is max(MMA, L2->SM operand bytes); 2-CTA tiles halve the W
+// bytes each SM loads.  AQB_GEMM_VARIANT=1cta256|1cta128|2cta256|2cta128
+// forces one (benchmarking).
+enum Variant { V1_256 = 0, V1_128, V2_256, V2_128 };
+
+static int pick_variant(int64_t m, int64_t n, int64_t k) {
+  static int forced = -2;
+  if (forced == -2) {
+    forced = -1;
+    if (const char* e = getenv("AQB_GEMM_VARIANT")) {
+      if (!strcmp(e, "1cta256")) forced = V1_256;
+      if (!strcmp(e, "1cta128")) forced = V1_128;
+      if (!strcmp(e, "2cta256")) forced = V2_256;
+      if (!strcmp(e, "2cta128")) forced = V2_128;
+    }
+  }
+  if (forced >= 0) return forced;
+  const double sms = sm_count();
+  struct C { int v, tm, tn, ctas; } cs[4] = {{V2_256, 256, 256, 2}, {V1_256, 128, 256, 1}, {V2_128, 256, 128, 2},
+                                             {V1_128, 128, 128, 1}};
+  double best = 1e30;
+  int bv = V2_256;
+  for (auto& c : cs) {
+    const double tiles = double((m + c.tm - 1) / c.tm) * double((n + c.tn - 1) / c.tn);
+    const double waves = std::ceil(tiles / (sms / c.ctas));
+    const double rows = c.tm / c.ctas;                        // A rows per SM
+    const double bytes = (rows + double(c.tn) / c.ctas) * 2;  // per SM per k
+    const double mma = rows * c.tn / 4096.0 * 0.5;            // cycles per SM per k
+    const double l2 = bytes / 64.0;                           // ~64 B/cycle/SM sustainable from L2
+    const double t = waves * std::max(mma, l2) * double(k);
+    if (t < best * 0.97) best = t, bv = c.v;
+  }
+  return bv;
 }
 
 }  // namespace gemm
@@ -305,8 +576,11 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
   AQB_CHECK_ARG(ldo >= n && ldo % 8 == 0, "gemm: bad ldo");
   AQB_CHECK_ARG(m < (1ll << 31) && n < (1ll << 31), "gemm: shape too large");
 
-  const int bn = pick_bn(m, n);
-  CUtensorMap ta, tb;
+  const int variant = pick_variant(m, n, k);
+  const bool pair = variant == V2_256 || variant == V2_128;
+  const int bn = (variant == V1_256 || variant == V2_256) ? 256 : 128;
+  const int tile_m = pair ? 2 * BM : BM;
+  CUtensorMap ta, tb, to;
   {
     uint64_t dims[2] = {uint64_t(k), uint64_t(m)};
     uint64_t strides[1] = {uint64_t(lda) * 2};
@@ -317,13 +591,25 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
   {
     uint64_t dims[2] = {uint64_t(k), uint64_t(n)};
     uint64_t strides[1] = {uint64_t(ldw) * 2};
-    uint32_t box[2] = {BK, uint32_t(bn)};
+    uint32_t box[2] = {BK, uint32_t(pair ? bn / 2 : bn)};
     int rc = make_tmap_bf16(&tb, w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  if (epilogue == AQB_EPI_EULER) {
+    memset(&to, 0, sizeof(to));  // direct stores; map unused
+  } else {
+    const bool f32 = epilogue == AQB_EPI_F32 || epilogue == AQB_EPI_GATE_RES;
+    const int esz = f32 ? 4 : 2;
+    uint64_t dims[2] = {uint64_t(n), uint64_t(m)};
+    uint64_t strides[1] = {uint64_t(ldo) * esz};
+    uint32_t box[2] = {uint32_t(128 / esz), uint32_t(BM)};
+    int rc = make_tmap(&to, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, 2, dims,
+                       strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
   }
   Params p{};
   p.M = int(m), p.N = int(n), p.K = int(k);
-  p.num_m = int((m + BM - 1) / BM);
+  p.num_m = int((m + tile_m - 1) / tile_m);
   p.num_n = int((n + bn - 1) / bn);
   p.num_tiles = p.num_m * p.num_n;
   p.group_m = 16;
@@ -331,6 +617,10 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
   p.aux = reinterpret_cast<__nv_bfloat16*>(aux), p.ld_aux = ld_aux;
   p.run_flag = run_flag, p.run_if = run_if;
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (bn == 256) return dispatch_epi<256, 4>(epilogue, ta, tb, p, s);
-  return dispatch_epi<128, 6>(epilogue, ta, tb, p, s);
+  switch (variant) {
+    case V1_256: return dispatch_epi<256, 4, false>(epilogue, ta, tb, to, p, s);
+    case V1_128: return dispatch_epi<128, 6, false>(epilogue, ta, tb, to, p, s);
+    case V2_256: return dispatch_epi<256, 6, true>(epilogue, ta, tb, to, p, s);
+    default: return dispatch_epi<128, 8, true>(epilogue, ta, tb, to, p, s);
+  }
 }

@@ -47,6 +47,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t* dims,
                    const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {
+  return make_tmap(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, base, rank, dims, strides_bytes, box, swz);
+}
+
+int make_tmap(CUtensorMap* map, CUtensorMapDataType dtype, const void* base, int rank, const uint64_t* dims,
+              const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle swz) {
   auto fn = encode_fn();
   if (!fn) return set_error(AQB_ECUDA, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   if (reinterpret_cast<uintptr_t>(base) % 16) return set_error(AQB_EINVAL, "TMA base pointer not 16B aligned");
@@ -61,7 +66,7 @@ int make_tmap_bf16(CUtensorMap* map, const void* base, int rank, const uint64_t*
       gstride[i - 1] = strides_bytes[i - 1];
     }
   }
-  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), gdim, gstride, bdim,
+  CUresult r = fn(map, dtype, rank, const_cast<void*>(base), gdim, gstride, bdim,
                   estride, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(AQB_ECUDA, "cuTensorMapEncodeTiled failed (CUresult %d)", int(r));

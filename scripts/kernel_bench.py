@@ -112,9 +112,12 @@ def main():
     args = ap.parse_args()
     res = []
     S, H = 7800, 2048
-    if args.only in ("all", "gemm"):
-        for (m, n, k, e) in [(S, 3 * H, H, "bf16"), (S, H, H, "gate_res"), (S, 4 * H, H, "gelu"), (S, H, 4 * H, "gate_res"),
-                             (14850 + 256, 3 * 3072, 3072, "bf16"), (8192, 8192, 8192, "bf16")]:
+    if args.only in ("all", "gemm", "gemm-proj"):
+        shapes = [(S, 3 * H, H, "bf16"), (S, H, H, "gate_res"), (S, 4 * H, H, "gelu"), (S, H, 4 * H, "gate_res"),
+                  (14850 + 256, 3 * 3072, 3072, "bf16"), (8192, 8192, 8192, "bf16")]
+        if args.only == "gemm-proj":
+            shapes = [(S, H, H, "bf16"), (S, H, H, "f32"), (S, H, H, "gate_res")]
+        for (m, n, k, e) in shapes:
             res.append(gemm_case(m, n, k, e, args.ncu))
     if args.only in ("all", "attn"):
         res.append(attn_case(S, S, 16, 128, args.ncu))
