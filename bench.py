@@ -165,6 +165,11 @@ def run_reference(args):
     return 0
 
 
+def _log(rank, msg):
+    if os.environ.get("AQB_BENCH_LOG"):
+        print(f"[bench r{rank} {time.strftime('%H:%M:%S')}] {msg}", file=sys.stderr, flush=True)
+
+
 # --------------------------------------------------------------------------- our arm
 def run_ours(args):
     from paper_2505_10584_b200 import SINGLE_DIT_2B, build_model, denoise, no_cache, plan_cache, flops_per_step
@@ -215,11 +220,13 @@ def run_ours(args):
 
     run_on = lambda: denoise(model, x0, steps, sched_on, graph=args.graph, graphs=graphs)  # noqa: E731
     run_off = lambda: denoise(model, x0, steps, sched_off, graph=args.graph, graphs=graphs)  # noqa: E731
+    _log(rank, "warmup")
     for _ in range(args.warmup):
         run_on()
     run_off()
     torch.cuda.synchronize()
 
+    _log(rank, "timed")
     clk = ClockSampler(local)
     clk.start()
     ms_on = timed(run_on, args.steps)
@@ -229,6 +236,7 @@ def run_ours(args):
     value_off = steps * max(1, args.steps) / (ms_off / 1e3)
 
     # e2e through the public API: pinned host latent in, host latent out
+    _log(rank, "e2e")
     x0_host = x0.cpu().pin_memory()
     out_bytes = x0_host.numel() * 4
 
@@ -249,6 +257,7 @@ def run_ours(args):
     e2e_value = steps * args.steps / float(e2e_t)
 
     # launch count of one video, then an instrumented (per-launch CUDA events) video
+    _log(rank, "profile")
     cnt = ops.KernelProfiler(timing=False)
     ops.set_profiler(cnt)
     denoise(model, x0, steps, sched_on)
@@ -314,10 +323,15 @@ def run_ours(args):
             line["cpu_baseline"] = {"value": c["steps_per_s_cache_on"], "unit": UNIT, "cores": threads, "kind": "port",
                                     "sample": c["sample"]}
         print(json.dumps(line), flush=True)
+    _log(rank, "done")
     if sp:
         dist.barrier()
-        dist.destroy_process_group()
-    return 0
+        torch.cuda.synchronize()
+    sys.stdout.flush()
+    sys.stderr.flush()
+    # NCCL communicators captured inside CUDA graphs can make process-group
+    # teardown block; the job's results are already printed, so exit hard.
+    os._exit(0)
 
 
 def main():

@@ -74,9 +74,27 @@ int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift, const flo
 #define AQB_EPI_GATE_RES 2
 #define AQB_EPI_F32 3
 #define AQB_EPI_EULER 4
+#define AQB_EPI_QKNORM_ROPE 5 /* internal: selected by aqb_gemm_qknorm_rope */
 int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t ldw, void* out, int64_t ldo, int64_t m,
                   int64_t n, int64_t k, const float* bias, const float* gate, int32_t epilogue, const float* alpha,
                   void* aux, int64_t ld_aux, const int32_t* run_flag, int32_t run_if, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * AllGather+QKV_Linear + Fused QKNorm + 3D RoPE in one kernel (PAPER.md:252-253,
+ * 114-115; memory.py:101,103): tcgen05 GEMM whose epilogue RMS-normalises each
+ * 128-wide head of the first norm_parts column parts (q_w, k_w), applies the 3D
+ * RoPE to rows with (rope_row0 + row) < rope_rows, and TMA-stores bf16 into
+ *   out[(h / hpg - g_base) * group_stride + row * out_row_stride
+ *       + part * hpg * 128 + (h % hpg) * 128 + d]
+ * (groups = Ulysses ranks; columns of heads whose group is outside
+ * [0, groups) are dropped).  head_dim must be 128; n = parts * part_width.
+ */
+int aqb_gemm_qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n, int64_t k,
+                         const float* bias, int32_t part_width, int32_t norm_parts, const float* q_w,
+                         const float* k_w, float eps, const float* rope_cos, const float* rope_sin,
+                         int64_t rope_row0, int64_t rope_rows, void* out, int64_t out_row_stride, int32_t groups,
+                         int64_t group_stride, int32_t hpg, int32_t g_base, const int32_t* run_flag,
+                         int32_t run_if, void* stream);
 
 /* ---------------------------------------------------------------------------
  * "Fused QKNorm" (memory.py:103) + 3D RoPE

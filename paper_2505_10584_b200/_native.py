@@ -25,6 +25,9 @@ SIGNATURES = {
     "aqb_norm_modulate": (c_int, [P, c_int64, P, P, P, c_int64, c_int64, c_int32, c_float, c_int32, P, P, P, c_int32, P]),
     "aqb_gemm_bf16": (c_int, [P, c_int64, P, c_int64, P, c_int64, c_int64, c_int64, c_int64, P, P, c_int32, P, P,
                               c_int64, P, c_int32, P]),
+    "aqb_gemm_qknorm_rope": (c_int, [P, c_int64, P, c_int64, c_int64, c_int64, c_int64, P, c_int32, c_int32, P, P,
+                                     c_float, P, P, c_int64, c_int64, P, c_int64, c_int32, c_int64, c_int32, c_int32,
+                                     P, c_int32, P]),
     "aqb_qk_norm_rope": (c_int, [P, c_int64, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, c_float, P, P, c_int64,
                                  c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, P, c_int32, P]),
     "aqb_attention_fwd": (c_int, [P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64,

@@ -53,6 +53,16 @@ struct Params {
   int64_t ld_aux;
   const int32_t* run_flag;
   int32_t run_if;
+  // QK-norm + RoPE epilogue (AQB_EPI_QKNORM_ROPE): columns are [parts][heads][128]
+  const float* norm_w0;   // q weight [128]
+  const float* norm_w1;   // k weight [128]
+  const float* rope_cos;  // [rope_rows, 64]
+  const float* rope_sin;
+  int64_t rope_row0, rope_rows;
+  int part_width;         // heads * 128
+  int norm_parts;         // parts < norm_parts are RMS-normed (+ RoPE)
+  int hpg, g_base, groups;  // heads per output group (Ulysses), group offset, group count
+  float eps;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int& nb) {
@@ -153,6 +163,89 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       euler_chunk(p, row0 + r, col_base + c, u);
     }
     return;
+  } else if constexpr (EPI == AQB_EPI_QKNORM_ROPE) {
+    // One 128-column head at a time: RMS-norm (+ RoPE) in registers, then two
+    // 64-column chunks through the swizzled smem buffers and a 5-D TMA store
+    // that lands in the [group][row][part][head][128] layout (natural or packed).
+#pragma unroll 1
+    for (int hc = 0; hc < BN; hc += 128) {
+      const int colh = col_base + hc;
+      if (colh >= p.N) break;
+      float v[128];
+      {
+        uint32_t u[32];
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+          tmem_ld32(tacc + hc + 32 * h + lane_off, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[32 * h + i] = __uint_as_float(u[i]);
+        }
+      }
+      if (p.bias != nullptr) {
+        const float4* b4 = reinterpret_cast<const float4*>(p.bias + colh);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float4 bb = __ldg(b4 + i);
+          v[4 * i] += bb.x, v[4 * i + 1] += bb.y, v[4 * i + 2] += bb.z, v[4 * i + 3] += bb.w;
+        }
+      }
+      const int part = colh / p.part_width;
+      const int head = (colh - part * p.part_width) >> 7;
+      const int grp = head / p.hpg - p.g_base;
+      if (grp < 0 || grp >= p.groups) continue;  // head not stored on this rank (TMA stores need coords >= 0)
+      if (part < p.norm_parts) {
+        float ss = 0.f;
+#pragma unroll
+        for (int i = 0; i < 128; ++i) ss += v[i] * v[i];
+        const float rstd = rsqrtf(ss * (1.f / 128.f) + p.eps);
+        const float4* w4 = reinterpret_cast<const float4*>(part == 0 ? p.norm_w0 : p.norm_w1);
+#pragma unroll
+        for (int i = 0; i < 32; ++i) {
+          const float4 w = __ldg(w4 + i);
+          v[4 * i] *= rstd * w.x, v[4 * i + 1] *= rstd * w.y, v[4 * i + 2] *= rstd * w.z, v[4 * i + 3] *= rstd * w.w;
+        }
+        const int64_t grow = p.rope_row0 + row0 + r;
+        if (grow < p.rope_rows) {
+          const float4* c4 = reinterpret_cast<const float4*>(p.rope_cos + grow * 64);
+          const float4* s4 = reinterpret_cast<const float4*>(p.rope_sin + grow * 64);
+#pragma unroll
+          for (int i = 0; i < 16; ++i) {
+            const float4 cc = __ldg(c4 + i), sn = __ldg(s4 + i);
+            const float cs[4] = {cc.x, cc.y, cc.z, cc.w}, sv[4] = {sn.x, sn.y, sn.z, sn.w};
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const int e = 8 * i + 2 * j;
+              const float a = v[e], b = v[e + 1];
+              v[e] = a * cs[j] - b * sv[j];
+              v[e + 1] = a * sv[j] + b * cs[j];
+            }
+          }
+        }
+      }
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        const uint32_t b = es.chunk & 1;
+        uint8_t* buf = es.buf + b * kEpiBuf;
+        if (leader_thread) bulk_wait_read<1>();
+        named_bar_sync(1, 128);
+        const uint32_t rowaddr = smem_u32(buf) + r * 128;
+        const uint32_t sw = r & 7;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float* t = v + 64 * half + 8 * i;
+          st_shared_v4(rowaddr + ((i ^ sw) << 4), pack_bf16(t[0], t[1]), pack_bf16(t[2], t[3]), pack_bf16(t[4], t[5]),
+                       pack_bf16(t[6], t[7]));
+        }
+        fence_proxy_async_smem();
+        named_bar_sync(1, 128);
+        if (leader_thread) {
+          tma_store_5d(tmo, buf, 64 * half, head % p.hpg, part, row0, grp);
+          bulk_commit();
+        }
+        ++es.chunk;
+      }
+    }
   } else {
     constexpr int NB = epi_bufs<EPI>();
     constexpr int CW = epi_cols<EPI>();  // columns per 128-byte chunk
@@ -516,6 +609,7 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
     case AQB_EPI_GATE_RES: return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, p, s);
     case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32, PAIR>(ta, tb, to, p, s);
     case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER, PAIR>(ta, tb, to, p, s);
+    case AQB_EPI_QKNORM_ROPE: return launch<BN, STAGES, AQB_EPI_QKNORM_ROPE, PAIR>(ta, tb, to, p, s);
   }
   return set_error(AQB_EINVAL, "unknown epilogue %d", epi);
 }
@@ -559,6 +653,46 @@ static int pick_variant(int64_t m, int64_t n, int64_t k) {
 }  // namespace gemm
 }  // namespace aqb
 
+namespace aqb {
+namespace gemm {
+
+// Shared host path: A/W tensor maps, variant choice, tile bookkeeping, launch.
+static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n, int64_t k, int epilogue,
+               Params& p, const CUtensorMap& to, int variant, cudaStream_t s) {
+  const bool pair = variant == V2_256 || variant == V2_128;
+  const int bn = (variant == V1_256 || variant == V2_256) ? 256 : 128;
+  const int tile_m = pair ? 2 * BM : BM;
+  CUtensorMap ta, tb;
+  {
+    uint64_t dims[2] = {uint64_t(k), uint64_t(m)};
+    uint64_t strides[1] = {uint64_t(lda) * 2};
+    uint32_t box[2] = {BK, BM};
+    int rc = make_tmap_bf16(&ta, a, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  {
+    uint64_t dims[2] = {uint64_t(k), uint64_t(n)};
+    uint64_t strides[1] = {uint64_t(ldw) * 2};
+    uint32_t box[2] = {BK, uint32_t(pair ? bn / 2 : bn)};
+    int rc = make_tmap_bf16(&tb, w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  p.M = int(m), p.N = int(n), p.K = int(k);
+  p.num_m = int((m + tile_m - 1) / tile_m);
+  p.num_n = int((n + bn - 1) / bn);
+  p.num_tiles = p.num_m * p.num_n;
+  p.group_m = 16;
+  switch (variant) {
+    case V1_256: return dispatch_epi<256, 4, false>(epilogue, ta, tb, to, p, s);
+    case V1_128: return dispatch_epi<128, 6, false>(epilogue, ta, tb, to, p, s);
+    case V2_256: return dispatch_epi<256, 6, true>(epilogue, ta, tb, to, p, s);
+    default: return dispatch_epi<128, 8, true>(epilogue, ta, tb, to, p, s);
+  }
+}
+
+}  // namespace gemm
+}  // namespace aqb
+
 extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t ldw, void* out, int64_t ldo,
                              int64_t m, int64_t n, int64_t k, const float* bias, const float* gate, int32_t epilogue,
                              const float* alpha, void* aux, int64_t ld_aux, const int32_t* run_flag, int32_t run_if,
@@ -577,24 +711,7 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
   AQB_CHECK_ARG(m < (1ll << 31) && n < (1ll << 31), "gemm: shape too large");
 
   const int variant = pick_variant(m, n, k);
-  const bool pair = variant == V2_256 || variant == V2_128;
-  const int bn = (variant == V1_256 || variant == V2_256) ? 256 : 128;
-  const int tile_m = pair ? 2 * BM : BM;
-  CUtensorMap ta, tb, to;
-  {
-    uint64_t dims[2] = {uint64_t(k), uint64_t(m)};
-    uint64_t strides[1] = {uint64_t(lda) * 2};
-    uint32_t box[2] = {BK, BM};
-    int rc = make_tmap_bf16(&ta, a, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (rc) return rc;
-  }
-  {
-    uint64_t dims[2] = {uint64_t(k), uint64_t(n)};
-    uint64_t strides[1] = {uint64_t(ldw) * 2};
-    uint32_t box[2] = {BK, uint32_t(pair ? bn / 2 : bn)};
-    int rc = make_tmap_bf16(&tb, w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
-    if (rc) return rc;
-  }
+  CUtensorMap to;
   if (epilogue == AQB_EPI_EULER) {
     memset(&to, 0, sizeof(to));  // direct stores; map unused
   } else {
@@ -608,19 +725,46 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
     if (rc) return rc;
   }
   Params p{};
-  p.M = int(m), p.N = int(n), p.K = int(k);
-  p.num_m = int((m + tile_m - 1) / tile_m);
-  p.num_n = int((n + bn - 1) / bn);
-  p.num_tiles = p.num_m * p.num_n;
-  p.group_m = 16;
   p.out = out, p.ldo = ldo, p.bias = bias, p.gate = gate, p.alpha = alpha;
   p.aux = reinterpret_cast<__nv_bfloat16*>(aux), p.ld_aux = ld_aux;
   p.run_flag = run_flag, p.run_if = run_if;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  switch (variant) {
-    case V1_256: return dispatch_epi<256, 4, false>(epilogue, ta, tb, to, p, s);
-    case V1_128: return dispatch_epi<128, 6, false>(epilogue, ta, tb, to, p, s);
-    case V2_256: return dispatch_epi<256, 6, true>(epilogue, ta, tb, to, p, s);
-    default: return dispatch_epi<128, 8, true>(epilogue, ta, tb, to, p, s);
+  return run(a, lda, w, ldw, m, n, k, epilogue, p, to, variant, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int aqb_gemm_qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n,
+                                    int64_t k, const float* bias, int32_t part_width, int32_t norm_parts,
+                                    const float* q_w, const float* k_w, float eps, const float* rope_cos,
+                                    const float* rope_sin, int64_t rope_row0, int64_t rope_rows, void* out,
+                                    int64_t out_row_stride, int32_t groups, int64_t group_stride, int32_t hpg,
+                                    int32_t g_base, const int32_t* run_flag, int32_t run_if, void* stream) {
+  using namespace aqb;
+  using namespace aqb::gemm;
+  AQB_CHECK_ARG(a && w && out, "gemm_qknorm_rope: null pointer");
+  AQB_CHECK_ARG(m >= 1 && k >= 1 && k % 8 == 0 && lda % 8 == 0 && ldw % 8 == 0, "gemm_qknorm_rope: bad shape");
+  AQB_CHECK_ARG(part_width >= 128 && part_width % 128 == 0 && n % part_width == 0 && n / part_width <= 3,
+                "gemm_qknorm_rope: columns must be [parts<=3][heads][128]");
+  AQB_CHECK_ARG(norm_parts >= 0 && norm_parts <= 2 && norm_parts <= n / part_width, "gemm_qknorm_rope: norm_parts");
+  AQB_CHECK_ARG(norm_parts < 1 || q_w, "gemm_qknorm_rope: q_w missing");
+  AQB_CHECK_ARG(norm_parts < 2 || k_w, "gemm_qknorm_rope: k_w missing");
+  AQB_CHECK_ARG(rope_rows <= 0 || (rope_cos && rope_sin), "gemm_qknorm_rope: rope tables missing");
+  AQB_CHECK_ARG(hpg >= 1 && groups >= 1 && out_row_stride % 8 == 0 && group_stride % 8 == 0,
+                "gemm_qknorm_rope: bad output layout");
+  const int parts = int(n / part_width);
+  CUtensorMap to;
+  {
+    // (d:128, head-in-group:hpg, part, row:m, group) ; strides in bytes
+    uint64_t dims[5] = {128, uint64_t(hpg), uint64_t(parts), uint64_t(m), uint64_t(groups)};
+    uint64_t strides[4] = {256, uint64_t(hpg) * 256, uint64_t(out_row_stride) * 2, uint64_t(group_stride) * 2};
+    uint32_t box[5] = {64, 1, 1, uint32_t(BM), 1};
+    int rc = make_tmap(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
   }
+  Params p{};
+  p.out = out, p.ldo = out_row_stride, p.bias = bias;
+  p.run_flag = run_flag, p.run_if = run_if;
+  p.norm_w0 = q_w, p.norm_w1 = k_w, p.rope_cos = rope_cos, p.rope_sin = rope_sin;
+  p.rope_row0 = rope_row0, p.rope_rows = rope_rows, p.part_width = part_width, p.norm_parts = norm_parts;
+  p.hpg = hpg, p.g_base = g_base, p.groups = groups, p.eps = eps;
+  return run(a, lda, w, ldw, m, n, k, AQB_EPI_QKNORM_ROPE, p, to, pick_variant(m, n, k),
+             reinterpret_cast<cudaStream_t>(stream));
 }

@@ -277,6 +277,13 @@ AQB_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int32_t x, int3
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+AQB_DEV void tma_store_5d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1, int32_t c2, int32_t c3,
+                          int32_t c4) {
+  asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
+               : "memory");
+}
 AQB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 AQB_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }

@@ -193,46 +193,80 @@ class DiTModel:
         n = 2 if name == "final.mod" else 6
         return [self.allmods[o + k * H:o + (k + 1) * H] for k in range(n)]
 
-    def _attention_self(self, p, r0, r1, rope, flag, run_if, txt=None):
-        """QK-norm/RoPE + joint self-attention over rows [r0, r1) (+ text rows for MM-DiT).
+    def _qkv_attention(self, pi, pt, flag, run_if):
+        """QKV projection(s) + QK-RMSNorm + 3D RoPE + joint self-attention -> self.o.
 
-        P == 1: in place on ``qkv``.  P > 1: Ulysses pack -> all-to-all ->
-        attention over A/P heads -> all-to-all back -> head->sequence repack.
-        ``p`` = weight prefix of the video (or only) stream, ``txt`` = text
-        stream prefix (dual blocks) or the same prefix (single blocks).
+        ``pi``: weight prefix of the video stream (rows [0, Sv_loc)); ``pt``:
+        prefix of the text rows [Sv_loc, rows) (MM-DiT; == pi for single
+        blocks) or None (Single-DiT).  head_dim 128 uses the fused
+        GEMM+norm+RoPE(+pack) kernel; other head dims run GEMM then
+        ``aqb_qk_norm_rope``.  P > 1 (Ulysses): the projection epilogue writes
+        the all-to-all send layout, text rows go straight into the receive
+        buffer's tail (local heads), attention runs over A/P heads and full
+        sequence, then the all-to-all back + head->sequence repack.
         """
         cfg, g, W = self.cfg, self.geo, self.W
         A, D, H, eps = cfg.num_heads, cfg.head_dim, cfg.hidden_size, cfg.qk_norm_eps
-        Sv_loc, St = g.Sv_loc, g.St
+        n, R, St = g.Sv_loc, g.rows, g.St
+        fused = D == 128
+        m, qkv = self.m, self.qkv
+        wi, bi = W[f"{pi}.qkv.w"], W[f"{pi}.qkv.b"]
+        if pt is not None:
+            wt, bt = W[f"{pt}.qkv.w"], W[f"{pt}.qkv.b"]
         if self.sp is None or self.sp.P == 1:
-            qv = self.qkv[r0:Sv_loc]
-            ops.qk_norm_rope(qv, A, D, W[f"{p}.q_norm"], W[f"{p}.k_norm"], eps, self.cos, self.sin, 0, g.Sv,
-                             run_flag=flag, run_if=run_if)
-            if St:
-                tp = txt or p
-                ops.qk_norm_rope(self.qkv[Sv_loc:], A, D, W[f"{tp}.q_norm"], W[f"{tp}.k_norm"], eps,
+            if fused:
+                if pt == pi or pt is None:
+                    ops.gemm_qknorm_rope(m, wi, qkv, H, 2, W[f"{pi}.q_norm"], W[f"{pi}.k_norm"], eps, bias=bi,
+                                         cos=self.cos, sin=self.sin, rope_rows=g.Sv, run_flag=flag, run_if=run_if)
+                else:
+                    ops.gemm_qknorm_rope(m[:n], wi, qkv[:n], H, 2, W[f"{pi}.q_norm"], W[f"{pi}.k_norm"], eps, bias=bi,
+                                         cos=self.cos, sin=self.sin, rope_rows=g.Sv, run_flag=flag, run_if=run_if)
+                    ops.gemm_qknorm_rope(m[n:], wt, qkv[n:], H, 2, W[f"{pt}.q_norm"], W[f"{pt}.k_norm"], eps, bias=bt,
+                                         run_flag=flag, run_if=run_if)
+            else:
+                if pt == pi or pt is None:
+                    ops.gemm(m, wi, qkv, bias=bi, run_flag=flag, run_if=run_if)
+                else:
+                    ops.gemm(m[:n], wi, qkv[:n], bias=bi, run_flag=flag, run_if=run_if)
+                    ops.gemm(m[n:], wt, qkv[n:], bias=bt, run_flag=flag, run_if=run_if)
+                ops.qk_norm_rope(qkv[:n], A, D, W[f"{pi}.q_norm"], W[f"{pi}.k_norm"], eps, self.cos, self.sin, 0, g.Sv,
                                  run_flag=flag, run_if=run_if)
-            q = self.qkv[r0:r1]
-            ops.attention(q, q[:, H:], q[:, 2 * H:], self.o[r0:r1], A, D, run_flag=flag, run_if=run_if)
+                if St:
+                    ops.qk_norm_rope(qkv[n:], A, D, W[f"{pt}.q_norm"], W[f"{pt}.k_norm"], eps, run_flag=flag,
+                                     run_if=run_if)
+            ops.attention(qkv, qkv[:, H:], qkv[:, 2 * H:], self.o, A, D, run_flag=flag, run_if=run_if)
             return
         sp, P, hl = self.sp, self.sp.P, self.hl
         snd, rcv = self.a2a_snd, self.a2a_rcv
-        ops.qk_norm_rope(self.qkv[:Sv_loc], A, D, W[f"{p}.q_norm"], W[f"{p}.k_norm"], eps, self.cos, self.sin,
-                         sp.rank * Sv_loc, g.Sv, dst=snd, hpg=hl, dst_group_stride=Sv_loc * 3 * hl * D,
-                         dst_row_stride=3 * hl * D, dst_which_stride=hl * D, run_flag=flag, run_if=run_if)
+        rs = 3 * hl * D  # row stride of the packed layouts
+        if fused:
+            ops.gemm_qknorm_rope(m[:n], wi, snd, H, 2, W[f"{pi}.q_norm"], W[f"{pi}.k_norm"], eps, bias=bi,
+                                 cos=self.cos, sin=self.sin, rope_row0=sp.rank * n, rope_rows=g.Sv, out_row_stride=rs,
+                                 groups=P, group_stride=n * rs, hpg=hl, run_flag=flag, run_if=run_if)
+        else:
+            ops.gemm(m[:n], wi, qkv[:n], bias=bi, run_flag=flag, run_if=run_if)
+            ops.qk_norm_rope(qkv[:n], A, D, W[f"{pi}.q_norm"], W[f"{pi}.k_norm"], eps, self.cos, self.sin,
+                             sp.rank * n, g.Sv, dst=snd, hpg=hl, dst_group_stride=n * rs, dst_row_stride=rs,
+                             dst_which_stride=hl * D, run_flag=flag, run_if=run_if)
         sp.all_to_all(rcv[:g.Sv].view(-1), snd.view(-1))
         if St:
-            tp = txt or p
-            ops.qk_norm_rope(self.qkv[Sv_loc:], A, D, W[f"{tp}.q_norm"], W[f"{tp}.k_norm"], eps,
-                             dst=rcv[g.Sv:].view(St, -1), head_begin=sp.rank * hl, head_count=hl, hpg=hl,
-                             dst_row_stride=3 * hl * D, dst_which_stride=hl * D, run_flag=flag, run_if=run_if)
+            tail = rcv[g.Sv:].view(St, -1)
+            if fused:
+                ops.gemm_qknorm_rope(m[n:], wt, tail, H, 2, W[f"{pt}.q_norm"], W[f"{pt}.k_norm"], eps, bias=bt,
+                                     out_row_stride=rs, groups=1, hpg=hl, g_base=sp.rank, run_flag=flag,
+                                     run_if=run_if)
+            else:
+                ops.gemm(m[n:], wt, qkv[n:], bias=bt, run_flag=flag, run_if=run_if)
+                ops.qk_norm_rope(qkv[n:], A, D, W[f"{pt}.q_norm"], W[f"{pt}.k_norm"], eps, dst=tail,
+                                 head_begin=sp.rank * hl, head_count=hl, hpg=hl, dst_row_stride=rs,
+                                 dst_which_stride=hl * D, run_flag=flag, run_if=run_if)
         q = rcv.view(g.Sv + St, -1)
         ops.attention(q, q[:, hl * D:], q[:, 2 * hl * D:], self.oh, hl, D, run_flag=flag, run_if=run_if)
         sp.all_to_all(self.ob.view(-1), self.oh[:g.Sv].reshape(-1))
-        ops.heads_to_seq(self.ob, Sv_loc, P, hl * D, self.o[:Sv_loc], run_flag=flag, run_if=run_if)
+        ops.heads_to_seq(self.ob, n, P, hl * D, self.o[:n], run_flag=flag, run_if=run_if)
         if St:
             sp.all_gather(self.tg.view(-1), self.oh[g.Sv:].reshape(-1))
-            ops.heads_to_seq(self.tg, St, P, hl * D, self.o[Sv_loc:], run_flag=flag, run_if=run_if)
+            ops.heads_to_seq(self.tg, St, P, hl * D, self.o[n:], run_flag=flag, run_if=run_if)
 
     def _mlp(self, p, r0, r1, mods, flag, run_if):
         """x += gate2 * fc2(gelu(fc1(norm_mod(x, shift2, scale2))))  on rows [r0, r1)."""
@@ -254,8 +288,7 @@ class DiTModel:
                           probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
         if probe:
             self._decide()
-        ops.gemm(self.m, W[f"{p}.qkv.w"], self.qkv, bias=W[f"{p}.qkv.b"], run_flag=flag, run_if=run_if)
-        self._attention_self(p, 0, n, True, flag, run_if)
+        self._qkv_attention(p, None, flag, run_if)
         ops.gemm(self.o, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=mods[2], epilogue="gate_res",
                  run_flag=flag, run_if=run_if)
         # cross-attention to the text (no norm before it, PixArt-α); K/V precomputed per call
@@ -279,9 +312,7 @@ class DiTModel:
         if probe:
             self._decide()
         ops.norm_modulate(self.x[n:], mt[0], mt[1], self.m[n:], eps, run_flag=flag, run_if=run_if)
-        ops.gemm(self.m[:n], W[f"{pi}.qkv.w"], self.qkv[:n], bias=W[f"{pi}.qkv.b"], run_flag=flag, run_if=run_if)
-        ops.gemm(self.m[n:], W[f"{pt}.qkv.w"], self.qkv[n:], bias=W[f"{pt}.qkv.b"], run_flag=flag, run_if=run_if)
-        self._attention_self(pi, 0, R, True, flag, run_if, txt=pt)
+        self._qkv_attention(pi, pt, flag, run_if)
         ops.gemm(self.o[:n], W[f"{pi}.proj.w"], self.x[:n], bias=W[f"{pi}.proj.b"], gate=mi[2], epilogue="gate_res",
                  run_flag=flag, run_if=run_if)
         ops.gemm(self.o[n:], W[f"{pt}.proj.w"], self.x[n:], bias=W[f"{pt}.proj.b"], gate=mt[2], epilogue="gate_res",
@@ -301,8 +332,7 @@ class DiTModel:
             ops.norm_modulate(self.x[n:], md[0], md[1], self.m[n:], eps, run_flag=flag, run_if=run_if)
         else:
             ops.norm_modulate(self.x, md[0], md[1], self.m, eps, run_flag=flag, run_if=run_if)
-        ops.gemm(self.m, W[f"{p}.qkv.w"], self.qkv, bias=W[f"{p}.qkv.b"], run_flag=flag, run_if=run_if)
-        self._attention_self(p, 0, R, True, flag, run_if)
+        self._qkv_attention(p, p, flag, run_if)
         ops.gemm(self.o, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=md[2], epilogue="gate_res",
                  run_flag=flag, run_if=run_if)
         self._mlp(p, 0, R, md, flag, run_if)

@@ -115,6 +115,25 @@ def gemm(a, w, out, bias=None, gate=None, epilogue="bf16", alpha=None, aux=None,
     return out
 
 
+def gemm_qknorm_rope(a, w, out, part_width, norm_parts, q_w, k_w, eps, bias=None, cos=None, sin=None, rope_row0=0,
+                     rope_rows=0, out_row_stride=None, groups=1, group_stride=0, hpg=None, g_base=0, run_flag=None,
+                     run_if=1):
+    """QKV projection with QK-RMSNorm + 3D RoPE (+ Ulysses pack) fused in the epilogue (head_dim 128)."""
+    _need(a, BF16, "gemm_qknorm_rope.a")
+    _need(w, BF16, "gemm_qknorm_rope.w")
+    _need(out, BF16, "gemm_qknorm_rope.out")
+    m, k = a.shape
+    n = w.shape[0]
+    hpg = part_width // 128 if hpg is None else hpg
+    if out_row_stride is None:
+        out_row_stride = out.stride(0)
+    _run("gemm", 2.0 * m * n * k, "aqb_gemm_qknorm_rope", _p(a), a.stride(0), _p(w), w.stride(0), m, n, k, _p(bias),
+         int(part_width), int(norm_parts), _p(q_w), _p(k_w), float(eps), _p(cos), _p(sin), int(rope_row0),
+         int(rope_rows), _p(out), int(out_row_stride), int(groups), int(group_stride), int(hpg), int(g_base),
+         _p(run_flag), int(run_if), _stream())
+    return out
+
+
 def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_row0=0, rope_rows=0,
                  dst=None, head_begin=0, head_count=None, hpg=None, dst_group_stride=0, dst_row_stride=None,
                  dst_which_stride=None, parts=3, norm_parts=2, run_flag=None, run_if=1):

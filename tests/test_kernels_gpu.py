@@ -230,3 +230,61 @@ def test_heads_to_seq():
     dst = torch.empty(rows, P * w, device=dev, dtype=torch.bfloat16)
     ops.heads_to_seq(src, rows, P, w, dst)
     assert torch.equal(dst, src.permute(1, 0, 2).reshape(rows, P * w))
+
+
+def _qkv_ref(a, w, b, qw, kw, heads, rope_rows, cos, sin, row0=0):
+    """fp32 statement: projection, per-head RMSNorm on q/k, RoPE on rows < rope_rows."""
+    x = (a.float() @ w.float().t() + b).cpu().view(a.shape[0], 3, heads, 128)
+    q = ref.rms_norm(x[:, 0], qw.cpu(), 1e-6)
+    k = ref.rms_norm(x[:, 1], kw.cpu(), 1e-6)
+    ang = torch.atan2(sin.cpu(), cos.cpu()).double()
+    n = max(0, min(a.shape[0], rope_rows - row0))
+    if n:
+        q = torch.cat([ref.apply_rope(q[:n], ang[row0:row0 + n]), q[n:]])
+        k = torch.cat([ref.apply_rope(k[:n], ang[row0:row0 + n]), k[n:]])
+    return torch.stack([q, k, x[:, 2]], dim=1)  # [rows, 3, heads, 128]
+
+
+@pytest.mark.parametrize("rows,heads", [(300, 2), (1000, 4), (7800, 16)])
+def test_gemm_qknorm_rope_natural_layout(rows, heads):
+    g = torch.Generator(device=dev).manual_seed(rows)
+    H = heads * 128
+    a = torch.randn(rows, H, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(3 * H, H, device=dev, generator=g) * 0.03).to(torch.bfloat16)
+    b = torch.randn(3 * H, device=dev, generator=g) * 0.1
+    qw = 1 + 0.1 * torch.randn(128, device=dev, generator=g)
+    kw = 1 + 0.1 * torch.randn(128, device=dev, generator=g)
+    ang = torch.rand(rows, 64, device=dev, generator=g) * 6.28
+    cos, sin = torch.cos(ang), torch.sin(ang)
+    rope_rows = rows - 7  # last rows (text-like) unrotated
+    out = torch.empty(rows, 3 * H, device=dev, dtype=torch.bfloat16)
+    ops.gemm_qknorm_rope(a, w, out, H, 2, qw, kw, 1e-6, bias=b, cos=cos, sin=sin, rope_rows=rope_rows)
+    exp = _qkv_ref(a, w, b, qw, kw, heads, rope_rows, cos, sin)
+    assert rel_l2(out.view(rows, 3, heads, 128), exp) < 6e-3
+
+
+def test_gemm_qknorm_rope_ulysses_pack_and_local_heads():
+    """Packed all-to-all send layout [P, rows, 3, hl, 128] and a local-heads-only (g_base) store."""
+    rows, heads, P = 500, 4, 2
+    hl, H = heads // P, heads * 128
+    g = torch.Generator(device=dev).manual_seed(9)
+    a = torch.randn(rows, H, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(3 * H, H, device=dev, generator=g) * 0.03).to(torch.bfloat16)
+    b = torch.randn(3 * H, device=dev, generator=g) * 0.1
+    qw = 1 + 0.1 * torch.randn(128, device=dev, generator=g)
+    kw = 1 + 0.1 * torch.randn(128, device=dev, generator=g)
+    ang = torch.rand(4 * rows, 64, device=dev, generator=g) * 6.28
+    cos, sin = torch.cos(ang), torch.sin(ang)
+    row0 = rows  # this rank's first global token
+    snd = torch.zeros(P, rows, 3, hl, 128, device=dev, dtype=torch.bfloat16)
+    ops.gemm_qknorm_rope(a, w, snd, H, 2, qw, kw, 1e-6, bias=b, cos=cos, sin=sin, rope_row0=row0,
+                         rope_rows=4 * rows, out_row_stride=3 * hl * 128, groups=P, group_stride=rows * 3 * hl * 128,
+                         hpg=hl)
+    exp = _qkv_ref(a, w, b, qw, kw, heads, 4 * rows, cos, sin, row0=row0)  # [rows, 3, heads, 128]
+    got = snd.permute(1, 2, 0, 3, 4).reshape(rows, 3, heads, 128)
+    assert rel_l2(got, exp) < 6e-3
+    # local heads only (group 1 of 2), no rope: other heads are dropped
+    loc = torch.zeros(rows, 3, hl, 128, device=dev, dtype=torch.bfloat16)
+    ops.gemm_qknorm_rope(a, w, loc, H, 2, qw, kw, 1e-6, bias=b, out_row_stride=3 * hl * 128, groups=1, hpg=hl, g_base=1)
+    exp2 = _qkv_ref(a, w, b, qw, kw, heads, 0, cos, sin)
+    assert rel_l2(loc, exp2[:, :, hl:]) < 6e-3
