@@ -171,6 +171,58 @@ def _log(rank, msg):
 
 
 # --------------------------------------------------------------------------- our arm
+def mmdit_720p(sp, timed, rank):
+    """North-star companion measurement: the 13.4B MM-DiT at BASELINE config 4's geometry
+    (129x720x1280 -> 118,800 video + 256 text tokens), cache on = plan_cache(50) (24 full / 26
+    cached).  One full and one cached step are timed (device events, max over ranks) after one
+    warm-up of each; steps/s of the 50-step video = 50 / (24 t_full + 26 t_cached).  One more
+    full step runs instrumented for the per-kernel table (joint-attention TFLOP/s)."""
+    from paper_2505_10584_b200 import MM_DIT_13B, build_model, flops_per_step, ops, plan_cache
+    from paper_2505_10584_b200.config import VIDEO_720P_129F
+    from paper_2505_10584_b200.weights import init_weights, synthetic_inputs
+
+    cfg = MM_DIT_13B
+    grid = VIDEO_720P_129F.grid(cfg)
+    steps = 50
+    sched = plan_cache(steps)
+    W = init_weights(cfg, seed=0, device="cuda")
+    inp = synthetic_inputs(cfg, grid, device="cuda")
+    model = build_model(cfg, weights=W, sp=sp).prepare(grid, inp["text"], inp["pooled"])
+    del W
+    torch.cuda.empty_cache()
+    model.reset(inp["x0"], steps)
+    model.step("full", True)
+    model.step("cached", True)
+    t_full = timed(lambda: model.step("full", True), 1)
+    t_cached = timed(lambda: model.step("cached", True), 1)
+    prof = ops.KernelProfiler(timing=True)
+    ops.set_profiler(prof)
+    model.step("full", True)
+    ops.set_profiler(None)
+    kinds = prof.summary()
+    tot = sum(d["ms"] for d in kinds.values())
+    n_full, n_cached = sched.full_steps, sched.cached_steps
+    video_ms = n_full * t_full + n_cached * t_cached
+    fl = flops_per_step(cfg, grid[0] * grid[1] * grid[2])
+    out = {
+        "workload": "config4: MM-DiT-13.4B (fitted H=3072 A=24, 25 dual + 29 single), 129x720x1280 -> 118,800 "
+                    "video + 256 text tokens, 50 Euler steps, cache on = plan_cache(50) (24 full / 26 cached)",
+        "value": steps / (video_ms / 1e3), "unit": "denoise_steps/s",
+        "ms_full_step": t_full, "ms_cached_step": t_cached,
+        "model_tflops_full_step": fl["total"] / (t_full / 1e3) / 1e12,
+        "kernels": {k: {"ms": round(v["ms"], 2), "share": round(v["ms"] / tot, 4),
+                        **({"tflops": round(v["work"] / (v["ms"] / 1e3) / 1e12, 1)}
+                           if k in ("gemm", "attention") else {})}
+                    for k, v in sorted(kinds.items(), key=lambda kv: -kv[1]["ms"])},
+    }
+    if "attention" in kinds:
+        a = kinds["attention"]
+        out["attention_tflops"] = a["work"] / (a["ms"] / 1e3) / 1e12
+    del model
+    torch.cuda.empty_cache()
+    return out
+
+
 def run_ours(args):
     from paper_2505_10584_b200 import SINGLE_DIT_2B, build_model, denoise, no_cache, plan_cache, flops_per_step
     from paper_2505_10584_b200 import ops
@@ -295,6 +347,12 @@ def run_ours(args):
     attn_tflops = attn["work"] / (attn["ms"] / 1e3) / 1e12 if attn else None
 
     fl = flops_per_step(cfg, grid[0] * grid[1] * grid[2])
+    mm = None
+    if not args.no_mmdit:
+        _log(rank, "mmdit 720p")
+        del model, graphs
+        torch.cuda.empty_cache()
+        mm = mmdit_720p(sp, timed, rank)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -304,6 +362,9 @@ def run_ours(args):
                                    "text 256x4096, 30 Euler steps, cache on = plan_cache(30) (17 full/13 cached); "
                                    "1 bench step = 1 video",
                        "parallelism": f"ulysses-sp{world}" if world > 1 else "single-gpu",
+                       "ulysses_exchange": (sp.exchange + (" (QKV-GEMM and attention epilogues store into peer "
+                                            "memory over NVLink; device barrier)" if sp.exchange == "p2p" else
+                                            " all_to_all")) if sp else None,
                        "l2": "inputs larger than L2 (4.3 GB of bf16 weights streamed per step)",
                        "cuda_graphs": bool(args.graph)},
             "cache_off": {"value": value_off, "unit": UNIT, "ms_per_video": ms_off / max(1, args.steps)},
@@ -317,6 +378,8 @@ def run_ours(args):
             "kernels": per_kind,
             "clocks": clocks,
         }
+        if mm is not None:
+            line["mmdit_720p"] = mm
         if world == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
             c = cpu_reference_sample(threads)
@@ -342,6 +405,7 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--no-mmdit", action="store_true", help="skip the 13.4B MM-DiT 720p companion measurement")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -29,7 +29,7 @@
 extern "C" {
 #endif
 
-#define AQB_ABI_VERSION 1
+#define AQB_ABI_VERSION 2
 
 #define AQB_OK 0
 #define AQB_EINVAL (-1)
@@ -96,6 +96,19 @@ int aqb_gemm_qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw,
                          int64_t group_stride, int32_t hpg, int32_t g_base, const int32_t* run_flag,
                          int32_t run_if, void* stream);
 
+/* Ulysses "AllGather+QKV_Linear" + "AlltoAll" fused: as
+ * aqb_gemm_qknorm_rope, but head group g (heads [g*hpg, (g+1)*hpg)) is
+ * TMA-stored straight into rank g's attention-input buffer: element
+ * (row, part, h, d) -> peer_out[g] + row*out_row_stride + part*hpg*128
+ * + (h % hpg)*128 + d.  peer_out: HOST array of nranks device pointers
+ * (peer memory), each already offset to this rank's row block. */
+int aqb_gemm_qknorm_rope_scatter(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n,
+                                 int64_t k, const float* bias, int32_t part_width, int32_t norm_parts,
+                                 const float* q_w, const float* k_w, float eps, const float* rope_cos,
+                                 const float* rope_sin, int64_t rope_row0, int64_t rope_rows, void* const* peer_out,
+                                 int32_t nranks, int64_t out_row_stride, int32_t hpg, const int32_t* run_flag,
+                                 int32_t run_if, void* stream);
+
 /* ---------------------------------------------------------------------------
  * "Fused QKNorm" (memory.py:103) + 3D RoPE
  * + Ulysses pack.  src bf16 [rows, parts, heads, D] (row stride ld_src), parts
@@ -120,11 +133,34 @@ int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t head
  * per head, tcgen05/TMEM, TMA-fed.  Rows of head h of Q start at
  * q + h*q_head_stride with row stride ldq (likewise K, V, O).  bf16 in/out;
  * f32 softmax statistics.  head_dim in {32, 64, 128}.  seq_kv >= 1.
+ * Split-KV (few heads x queries vs. 148 SMs, e.g. Ulysses' A/P heads):
+ * kv_splits = 0 picks the split count (aqb_attention_splits), 1 disables it;
+ * the partials (f32 O/l + log2-sum-exp2 per row) go to `workspace`
+ * (aqb_attention_workspace_bytes) and a combine pass writes O.  Automatic
+ * splitting silently stays at 1 split without enough workspace.
  */
 int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const void* k, int64_t ldk,
                       int64_t k_head_stride, const void* v, int64_t ldv, int64_t v_head_stride, void* o,
                       int64_t ldo, int64_t o_head_stride, int64_t seq_q, int64_t seq_kv, int32_t heads,
-                      int32_t head_dim, float softmax_scale, const int32_t* run_flag, int32_t run_if, void* stream);
+                      int32_t head_dim, float softmax_scale, int32_t kv_splits, void* workspace,
+                      int64_t workspace_bytes, const int32_t* run_flag, int32_t run_if, void* stream);
+int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
+int64_t aqb_attention_workspace_bytes(int64_t seq_q, int32_t heads, int32_t head_dim, int32_t kv_splits);
+
+/* Ulysses "AlltoAll after attention" fused into the attention epilogue
+ * (comm.py:65-96 costs it): output row r < text_row0 of head h
+ * is stored into rank (r / rows_per_rank)'s O buffer, row r % rows_per_rank:
+ *   peer_o[r / rows_per_rank] + h*o_head_stride + (r % rows_per_rank)*ldo + d;
+ * rows r >= text_row0 (replicated text tokens) go to every rank at row
+ * rows_per_rank + (r - text_row0).  peer_o is a HOST array of nranks device
+ * pointers (peer memory, see aqb_peer_open), each already offset to this
+ * rank's head columns.  text_row0 == rows_per_rank * nranks. */
+int aqb_attention_fwd_scatter(const void* q, int64_t ldq, int64_t q_head_stride, const void* k, int64_t ldk,
+                              int64_t k_head_stride, const void* v, int64_t ldv, int64_t v_head_stride,
+                              void* const* peer_o, int32_t nranks, int64_t ldo, int64_t o_head_stride,
+                              int64_t rows_per_rank, int64_t text_row0, int64_t seq_q, int64_t seq_kv, int32_t heads,
+                              int32_t head_dim, float softmax_scale, int32_t kv_splits, void* workspace,
+                              int64_t workspace_bytes, const int32_t* run_flag, int32_t run_if, void* stream);
 
 /* ---------------------------------------------------------------------------
  * AdaLN / timestep GEMV (tiny, per step):  y[n] = act(sum_k W[n,k] * in(x[k]) + b[n]) + add[n]
@@ -169,6 +205,58 @@ int aqb_unpatchify(const float* tok, float* lat, int32_t C, int32_t T, int32_t H
 /* Ulysses head->sequence repack: src bf16 [P, rows, hpg*D] -> dst [rows, P*hpg*D] (row stride ld_dst). */
 int aqb_heads_to_seq(const void* src, int64_t rows, int32_t P, int32_t width, void* dst, int64_t ld_dst,
                      const int32_t* run_flag, int32_t run_if, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * fp32 validation mode (north_star: <= 1e-4 latent rel-L2 vs the CPU
+ * reference).  Same semantics as the bf16 entries above with every activation
+ * in f32: aqb_norm_modulate_f32 writes f32 y; aqb_qk_norm_rope_f32 reads and
+ * writes f32; aqb_gemm_f32 takes f32 A, the bf16 weight W, and always writes
+ * f32 (AQB_EPI_BF16 / AQB_EPI_GELU_BF16 produce f32 here; aux of EULER is f32);
+ * aqb_attention_f32 is f32 in/out with exact expf.  SIMT kernels for the
+ * validation geometries, not the production path.
+ */
+int aqb_norm_modulate_f32(const float* x, int64_t ldx, const float* shift, const float* scale, float* y, int64_t ldy,
+                          int64_t rows, int32_t hidden, float eps, int32_t norm_kind, float* probe_prev,
+                          float* probe_partials, const int32_t* run_flag, int32_t run_if, void* stream);
+int aqb_qk_norm_rope_f32(const float* src, int64_t ld_src, int64_t rows, int32_t heads, int32_t head_begin,
+                         int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
+                         const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows, float* dst,
+                         int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride, int32_t hpg,
+                         int32_t parts, int32_t norm_parts, const int32_t* run_flag, int32_t run_if, void* stream);
+int aqb_gemm_f32(const float* a, int64_t lda, const void* w, int64_t ldw, float* out, int64_t ldo, int64_t m,
+                 int64_t n, int64_t k, const float* bias, const float* gate, int32_t epilogue, const float* alpha,
+                 float* aux, int64_t ld_aux, const int32_t* run_flag, int32_t run_if, void* stream);
+int aqb_attention_f32(const float* q, int64_t ldq, int64_t q_head_stride, const float* k, int64_t ldk,
+                      int64_t k_head_stride, const float* v, int64_t ldv, int64_t v_head_stride, float* o, int64_t ldo,
+                      int64_t o_head_stride, int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim,
+                      float softmax_scale, const int32_t* run_flag, int32_t run_if, void* stream);
+
+/* ---------------------------------------------------------------------------
+ * Peer memory over NVLink/NVSwitch (one process per GPU; the Ulysses exchange).
+ * aqb_peer_alloc: zeroed device allocation + its CUDA IPC handle
+ *   (AQB_IPC_HANDLE_BYTES bytes, exchanged by the caller, e.g. torch.distributed).
+ * aqb_peer_open / aqb_peer_close: map / unmap another rank's allocation.
+ * aqb_peer_barrier: stream-ordered barrier of nranks ranks.  peer_signal is a
+ *   HOST array of nranks device pointers to each rank's AQB_PEER_SIGNAL_BYTES
+ *   signal region (peer memory, zeroed); epoch is this rank's device counter
+ *   (uint32, starts at 0, advanced by every barrier).  All prior writes of this
+ *   rank (incl. stores into peer memory by earlier kernels) are visible to every
+ *   rank after the barrier.  With npay > 0 (<= 4) each rank contributes
+ *   payload[0:npay] and pay_out receives the sum over ranks in rank order
+ *   (bit-identical on every rank).  A peer missing for ~10 s sets *status = 1
+ *   and the kernel returns (no hang).  Gated by run_flag like the compute kernels
+ *   (every rank must take the same gate decisions).
+ */
+#define AQB_IPC_HANDLE_BYTES 64
+#define AQB_PEER_SIGNAL_BYTES 512
+int aqb_peer_alloc(int64_t bytes, void** ptr, void* ipc_handle);
+int aqb_peer_open(const void* ipc_handle, void** ptr);
+int aqb_peer_close(void* ptr);
+int aqb_peer_free(void* ptr);
+int aqb_peer_can_access(int32_t device, int32_t peer_device);
+int aqb_peer_barrier(void* const* peer_signal, int32_t rank, int32_t nranks, uint32_t* epoch, const float* payload,
+                     int32_t npay, float* pay_out, int32_t* status, const int32_t* run_flag, int32_t run_if,
+                     void* stream);
 
 #ifdef __cplusplus
 }

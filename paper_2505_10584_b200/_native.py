@@ -31,7 +31,30 @@ SIGNATURES = {
     "aqb_qk_norm_rope": (c_int, [P, c_int64, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, c_float, P, P, c_int64,
                                  c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, P, c_int32, P]),
     "aqb_attention_fwd": (c_int, [P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64,
-                                  c_int64, c_int64, c_int32, c_int32, c_float, P, c_int32, P]),
+                                  c_int64, c_int64, c_int32, c_int32, c_float, c_int32, P, c_int64, P, c_int32, P]),
+    "aqb_attention_splits": (c_int, [c_int64, c_int64, c_int32, c_int32]),
+    "aqb_attention_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int32]),
+    "aqb_attention_fwd_scatter": (c_int, [P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int32,
+                                          c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int32, c_int32,
+                                          c_float, c_int32, P, c_int64, P, c_int32, P]),
+    "aqb_gemm_qknorm_rope_scatter": (c_int, [P, c_int64, P, c_int64, c_int64, c_int64, c_int64, P, c_int32, c_int32,
+                                             P, P, c_float, P, P, c_int64, c_int64, P, c_int32, c_int64, c_int32, P,
+                                             c_int32, P]),
+    "aqb_norm_modulate_f32": (c_int, [P, c_int64, P, P, P, c_int64, c_int64, c_int32, c_float, c_int32, P, P, P,
+                                      c_int32, P]),
+    "aqb_qk_norm_rope_f32": (c_int, [P, c_int64, c_int64, c_int32, c_int32, c_int32, c_int32, P, P, c_float, P, P,
+                                     c_int64, c_int64, P, c_int64, c_int64, c_int64, c_int32, c_int32, c_int32, P,
+                                     c_int32, P]),
+    "aqb_gemm_f32": (c_int, [P, c_int64, P, c_int64, P, c_int64, c_int64, c_int64, c_int64, P, P, c_int32, P, P,
+                             c_int64, P, c_int32, P]),
+    "aqb_attention_f32": (c_int, [P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64,
+                                  c_int64, c_int64, c_int64, c_int32, c_int32, c_float, P, c_int32, P]),
+    "aqb_peer_alloc": (c_int, [c_int64, P, P]),
+    "aqb_peer_open": (c_int, [P, P]),
+    "aqb_peer_close": (c_int, [P]),
+    "aqb_peer_free": (c_int, [P]),
+    "aqb_peer_can_access": (c_int, [c_int32, c_int32]),
+    "aqb_peer_barrier": (c_int, [P, c_int32, c_int32, P, P, c_int32, P, P, P, c_int32, P]),
     "aqb_gemv": (c_int, [P, P, P, P, P, P, c_int64, c_int64, c_int32, P]),
     "aqb_add_bcast": (c_int, [P, P, c_int64, P, c_int64, P]),
     "aqb_rel_l1_reduce": (c_int, [P, c_int64, P, P]),
@@ -72,6 +95,16 @@ def load():
         fn.argtypes = args
     _lib = lib
     return lib
+
+
+def query(name: str, *args):
+    """Call a pure host-side query (returns its value; no status code)."""
+    return getattr(load(), name)(*args)
+
+
+def ptr_array(ptrs):
+    """HOST array of device pointers (``void* const*`` arguments)."""
+    return (c_void_p * len(ptrs))(*[int(p) for p in ptrs])
 
 
 def call(name: str, *args) -> None:

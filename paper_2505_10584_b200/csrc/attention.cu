@@ -21,6 +21,7 @@
 //               K-major layout the MMA reads; final 1/l normalisation and
 //               bf16 store from the same warps.
 // TMEM: S0 | S1 | O0 | O1  (128 + 128 + D + D columns).
+#include <algorithm>
 #include <cmath>
 
 #include "host.cuh"
@@ -50,14 +51,49 @@ struct Cfg {
   static constexpr int kBoxes = D / 64;                      // 64-column TMA boxes per row
 };
 
+constexpr int kMaxPeers = 8;
+
+// Where output row `row` of head `head` lands.  Local: o + head*ohs + row*ldo.
+// Ulysses scatter (nranks > 0): video row `row` belongs to rank row / rpr and
+// goes straight into that rank's O buffer (peer memory over NVLink) at row
+// row % rpr; text rows (row >= text_row0) are replicated into every rank's
+// buffer after its rpr video rows.  peer_o[r] already points at this rank's
+// head-column slice of rank r's buffer.
+struct OutMap {
+  __nv_bfloat16* o;
+  int64_t ldo, o_head_stride;
+  __nv_bfloat16* peer_o[kMaxPeers];
+  int nranks;
+  int64_t rows_per_rank, text_row0;
+};
+
 struct Params {
   int seq_q, seq_kv, heads, head_dim;
   float scale_log2;
-  __nv_bfloat16* o;
-  int64_t ldo, o_head_stride;
+  OutMap out;
+  int splits, kv_blocks_per_split;  // split-KV: blockIdx.z = split; partials go to opart/lse
+  float* opart;                     // [splits][heads][seq_q][head_dim] f32 (O / l of the split)
+  float* lse;                       // [splits][heads][seq_q] f32, log2-sum-exp2 of the split
+  int part_d;                       // row stride of opart (the kernel's D)
   const int32_t* run_flag;
   int32_t run_if;
 };
+
+// Calls fn(ptr) for every destination of (head, row): one, or all ranks for
+// replicated text rows under the Ulysses scatter.
+template <typename F>
+__device__ __forceinline__ void for_each_out(const OutMap& m, int head, int64_t row, F&& fn) {
+  const int64_t hoff = static_cast<int64_t>(head) * m.o_head_stride;
+  if (m.nranks == 0) {
+    fn(m.o + hoff + row * m.ldo);
+  } else if (row < m.text_row0) {
+    const int r = int(row / m.rows_per_rank);
+    fn(m.peer_o[r] + hoff + (row - r * m.rows_per_rank) * m.ldo);
+  } else {
+    const int64_t lr = m.rows_per_rank + (row - m.text_row0);
+    for (int r = 0; r < m.nranks; ++r) fn(m.peer_o[r] + hoff + lr * m.ldo);
+  }
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -82,7 +118,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_idx(), lane = lane_idx();
   const int head = blockIdx.y;
   const int q0 = blockIdx.x * (2 * BQ);
-  const int nkv = (p.seq_kv + BKV - 1) / BKV;
+  const int split = blockIdx.z;
+  const int j0 = split * p.kv_blocks_per_split;  // first KV block of this split
+  const int nkv = min((p.seq_kv + BKV - 1) / BKV - j0, p.kv_blocks_per_split);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
@@ -120,7 +158,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(kv_empty + s, ph ^ 1);
         mbar_arrive_expect_tx(kv_full + s, C::kKVBytes);
         const CUtensorMap* m = (i & 1) ? &tv : &tk;
-        const int row = (i >> 1) * BKV;
+        const int row = (j0 + (i >> 1)) * BKV;
         for (int c = 0; c < C::kBoxes; ++c)
           tma_load_3d(sKV + s * C::kKVBytes + c * (BKV * 128), m, kv_full + s, c * 64, head, row, kEvictLast);
       }
@@ -208,7 +246,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld64(s_tmem, sr);
       tmem_ld64(s_tmem + 64, sr + 64);
       tmem_wait_ld();
-      const int kv_valid = p.seq_kv - j * BKV;
+      const int kv_valid = p.seq_kv - (j0 + j) * BKV;
       if (kv_valid < BKV) {
 #pragma unroll
         for (int i = 0; i < BKV; ++i)
@@ -285,25 +323,47 @@ __global__ void __launch_bounds__(kThreads, 1)
       tc_fence_before();
       mbar_arrive(p_full + t);
     }
-    // epilogue: O / l -> bf16
+    // epilogue: O / l -> bf16 (or the split's f32 partial + log2-sum-exp2)
     mbar_wait(o_ready + t, (nkv - 1) & 1);
     tc_fence_after();
     const int row = q0 + t * BQ + r;
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    __nv_bfloat16* orow = p.o + static_cast<int64_t>(head) * p.o_head_stride + static_cast<int64_t>(row) * p.ldo;
+    const bool live = row < p.seq_q;
+    if (p.splits > 1) {
+      const int64_t prow = (static_cast<int64_t>(split) * p.heads + head) * p.seq_q + row;
+      if (live) p.lse[prow] = m_run * c + __log2f(l_run);
+      float* orow = p.opart + prow * D;
 #pragma unroll 1
-    for (int cc = 0; cc < D / 32; ++cc) {
-      uint32_t u[32];
-      tmem_ld32(o_tmem + cc * 32, u);
-      tmem_wait_ld();
-      if (row < p.seq_q && cc * 32 < p.head_dim) {
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t u[32];
+        tmem_ld32(o_tmem + cc * 32, u);
+        tmem_wait_ld();
+        if (live) {
 #pragma unroll
-        for (int g = 0; g < 4; ++g) {
-          const uint4 pk = make_uint4(pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
-                                      pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
-                                      pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
-                                      pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
-          *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = pk;
+          for (int g = 0; g < 8; ++g)
+            *reinterpret_cast<float4*>(orow + cc * 32 + 4 * g) =
+                make_float4(__uint_as_float(u[4 * g]) * inv, __uint_as_float(u[4 * g + 1]) * inv,
+                            __uint_as_float(u[4 * g + 2]) * inv, __uint_as_float(u[4 * g + 3]) * inv);
+        }
+      }
+    } else {
+#pragma unroll 1
+      for (int cc = 0; cc < D / 32; ++cc) {
+        uint32_t u[32];
+        tmem_ld32(o_tmem + cc * 32, u);
+        tmem_wait_ld();
+        if (live && cc * 32 < p.head_dim) {
+          uint4 pk[4];
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            pk[g] = make_uint4(pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
+                               pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
+                               pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
+                               pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
+          for_each_out(p.out, head, row, [&](__nv_bfloat16* orow) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = pk[g];
+          });
         }
       }
     }
@@ -316,6 +376,55 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+}
+
+// Split-KV combine: one warp per (row, head); lane owns 4 of the D columns.
+//   O = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M),  M = max_s lse_s
+__global__ void __launch_bounds__(256) attn_combine_kernel(Params p) {
+  if (!gate_open(p.run_flag, p.run_if)) return;
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= static_cast<int64_t>(p.seq_q) * p.heads) return;
+  const int head = int(w % p.heads);
+  const int64_t row = w / p.heads;
+  const int64_t plane = static_cast<int64_t>(p.heads) * p.seq_q;
+  const int64_t base = static_cast<int64_t>(head) * p.seq_q + row;
+  float mx = -INFINITY;
+  for (int s = 0; s < p.splits; ++s) mx = fmaxf(mx, p.lse[s * plane + base]);
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  float den = 0.f;
+  const int D = p.head_dim, PD = p.part_d;
+  for (int s = 0; s < p.splits; ++s) {
+    const float wt = exp2f(p.lse[s * plane + base] - mx);
+    den += wt;
+    if (lane * 4 < D) {
+      const float4 v = *reinterpret_cast<const float4*>(p.opart + (s * plane + base) * PD + lane * 4);
+      acc.x += wt * v.x, acc.y += wt * v.y, acc.z += wt * v.z, acc.w += wt * v.w;
+    }
+  }
+  if (lane * 4 >= D) return;
+  const float inv = 1.f / den;
+  const uint2 pk = make_uint2(pack_bf16(acc.x * inv, acc.y * inv), pack_bf16(acc.z * inv, acc.w * inv));
+  for_each_out(p.out, head, row, [&](__nv_bfloat16* orow) { *reinterpret_cast<uint2*>(orow + lane * 4) = pk; });
+}
+
+// KV splits for a launch: minimise waves x (KV blocks per split + fixed cost)
+// plus the combine pass's traffic, expressed in KV-block units (~2.3 us per
+// 256-query block on one SM at ~1.1 PFLOP/s device-wide).
+int choose_splits(int64_t seq_q, int64_t seq_kv, int heads, int head_dim) {
+  const int nkv = int((seq_kv + BKV - 1) / BKV);
+  const int64_t units = ((seq_q + 2 * BQ - 1) / (2 * BQ)) * heads;
+  const double sms = sm_count();
+  double best = 1e30;
+  int bs = 1;
+  for (int s = 1; s <= 16 && s <= nkv / 2 + (s == 1); ++s) {
+    const int per = (nkv + s - 1) / s;
+    const double waves = std::ceil(double(units) * s / sms);
+    double t = waves * (per + 2.0);
+    if (s > 1) t += double(s) * seq_q * heads * (head_dim * 4 + 4) * 2.0 / 5e12 / 2.3e-6 + 1.0;
+    if (t < best * 0.95) best = t, bs = s;
+  }
+  return bs;
 }
 
 template <int D>
@@ -347,34 +456,112 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     AQB_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
-  dim3 grid((p.seq_q + 2 * BQ - 1) / (2 * BQ), p.heads);
+  dim3 grid((p.seq_q + 2 * BQ - 1) / (2 * BQ), p.heads, p.splits);
   attn_fwd_kernel<D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
   AQB_LAUNCH_CHECK();
+  if (p.splits > 1) {
+    const int64_t warps = static_cast<int64_t>(p.seq_q) * p.heads;
+    attn_combine_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, stream>>>(p);
+    AQB_LAUNCH_CHECK();
+  }
   return AQB_OK;
 }
 
 }  // namespace attn
 }  // namespace aqb
 
-extern "C" int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const void* k, int64_t ldk,
-                                 int64_t k_head_stride, const void* v, int64_t ldv, int64_t v_head_stride, void* o,
-                                 int64_t ldo, int64_t o_head_stride, int64_t seq_q, int64_t seq_kv, int32_t heads,
-                                 int32_t head_dim, float softmax_scale, const int32_t* run_flag, int32_t run_if,
-                                 void* stream) {
-  using namespace aqb;
-  AQB_CHECK_ARG(q && k && v && o, "attention: null pointer");
+namespace aqb {
+namespace attn {
+
+static int run(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, int64_t khs, const void* v,
+               int64_t ldv, int64_t vhs, int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim,
+               float softmax_scale, int32_t kv_splits, void* workspace, int64_t workspace_bytes, const OutMap& om,
+               const int32_t* run_flag, int32_t run_if, cudaStream_t s) {
+  AQB_CHECK_ARG(q && k && v, "attention: null pointer");
   AQB_CHECK_ARG(head_dim == 32 || head_dim == 64 || head_dim == 128, "attention: head_dim %d unsupported", head_dim);
   AQB_CHECK_ARG(seq_q >= 1 && seq_kv >= 1 && heads >= 1, "attention: bad shape");
   AQB_CHECK_ARG(seq_q < (1ll << 31) && seq_kv < (1ll << 31), "attention: sequence too long");
-  AQB_CHECK_ARG(ldq % 8 == 0 && ldk % 8 == 0 && ldv % 8 == 0 && ldo % 8 == 0, "attention: rows must be 16B aligned");
-  AQB_CHECK_ARG(q_head_stride % 8 == 0 && k_head_stride % 8 == 0 && v_head_stride % 8 == 0 && o_head_stride % 8 == 0,
+  AQB_CHECK_ARG(ldq % 8 == 0 && ldk % 8 == 0 && ldv % 8 == 0 && om.ldo % 8 == 0, "attention: rows must be 16B aligned");
+  AQB_CHECK_ARG(qhs % 8 == 0 && khs % 8 == 0 && vhs % 8 == 0 && om.o_head_stride % 8 == 0,
                 "attention: head strides must be 16B aligned");
-  attn::Params p{};
+  const int nkv = int((seq_kv + BKV - 1) / BKV);
+  int splits = kv_splits > 0 ? kv_splits : choose_splits(seq_q, seq_kv, heads, head_dim);
+  splits = std::min(splits, nkv);
+  const int per = (nkv + splits - 1) / splits;
+  splits = (nkv + per - 1) / per;  // no empty split
+  if (splits > 1) {
+    const int64_t need = aqb_attention_workspace_bytes(seq_q, heads, head_dim, splits);
+    if (workspace == nullptr || workspace_bytes < need) {
+      AQB_CHECK_ARG(kv_splits <= 1, "attention: workspace of %lld B needed for %d splits", (long long)need, splits);
+      splits = 1;  // automatic choice without (enough) workspace: one pass
+    }
+  }
+  Params p{};
   p.seq_q = int(seq_q), p.seq_kv = int(seq_kv), p.heads = heads, p.head_dim = head_dim;
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
-  p.o = reinterpret_cast<__nv_bfloat16*>(o), p.ldo = ldo, p.o_head_stride = o_head_stride;
+  p.out = om;
+  p.splits = splits;
+  p.kv_blocks_per_split = splits > 1 ? per : nkv;
+  p.part_d = head_dim <= 64 ? 64 : 128;
+  if (splits > 1) {
+    float* ws = reinterpret_cast<float*>(workspace);
+    p.lse = ws;
+    const int64_t lse_elems = (static_cast<int64_t>(splits) * heads * seq_q + 63) / 64 * 64;
+    p.opart = ws + lse_elems;
+  }
   p.run_flag = run_flag, p.run_if = run_if;
-  cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (head_dim == 128) return attn::launch<128>(q, ldq, q_head_stride, k, ldk, k_head_stride, v, ldv, v_head_stride, p, s);
-  return attn::launch<64>(q, ldq, q_head_stride, k, ldk, k_head_stride, v, ldv, v_head_stride, p, s);
+  if (head_dim == 128) return launch<128>(q, ldq, qhs, k, ldk, khs, v, ldv, vhs, p, s);
+  return launch<64>(q, ldq, qhs, k, ldk, khs, v, ldv, vhs, p, s);
+}
+
+}  // namespace attn
+}  // namespace aqb
+
+extern "C" int64_t aqb_attention_workspace_bytes(int64_t seq_q, int32_t heads, int32_t head_dim, int32_t kv_splits) {
+  if (kv_splits <= 1) return 0;
+  const int64_t rows = static_cast<int64_t>(kv_splits) * heads * seq_q;
+  const int64_t d = head_dim <= 64 ? 64 : head_dim;
+  return ((rows + 63) / 64 * 64 + rows * d) * 4;
+}
+
+extern "C" int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim) {
+  return aqb::attn::choose_splits(seq_q, seq_kv, heads, head_dim);
+}
+
+extern "C" int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const void* k, int64_t ldk,
+                                 int64_t k_head_stride, const void* v, int64_t ldv, int64_t v_head_stride, void* o,
+                                 int64_t ldo, int64_t o_head_stride, int64_t seq_q, int64_t seq_kv, int32_t heads,
+                                 int32_t head_dim, float softmax_scale, int32_t kv_splits, void* workspace,
+                                 int64_t workspace_bytes, const int32_t* run_flag, int32_t run_if, void* stream) {
+  using namespace aqb;
+  AQB_CHECK_ARG(o, "attention: null output");
+  attn::OutMap om{};
+  om.o = reinterpret_cast<__nv_bfloat16*>(o), om.ldo = ldo, om.o_head_stride = o_head_stride;
+  return attn::run(q, ldq, q_head_stride, k, ldk, k_head_stride, v, ldv, v_head_stride, seq_q, seq_kv, heads,
+                   head_dim, softmax_scale, kv_splits, workspace, workspace_bytes, om, run_flag, run_if,
+                   reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int aqb_attention_fwd_scatter(const void* q, int64_t ldq, int64_t q_head_stride, const void* k,
+                                         int64_t ldk, int64_t k_head_stride, const void* v, int64_t ldv,
+                                         int64_t v_head_stride, void* const* peer_o, int32_t nranks, int64_t ldo,
+                                         int64_t o_head_stride, int64_t rows_per_rank, int64_t text_row0,
+                                         int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim,
+                                         float softmax_scale, int32_t kv_splits, void* workspace,
+                                         int64_t workspace_bytes, const int32_t* run_flag, int32_t run_if,
+                                         void* stream) {
+  using namespace aqb;
+  AQB_CHECK_ARG(peer_o && nranks >= 1 && nranks <= attn::kMaxPeers, "attention_scatter: 1..%d ranks", attn::kMaxPeers);
+  AQB_CHECK_ARG(rows_per_rank >= 1 && text_row0 == rows_per_rank * nranks && text_row0 <= seq_q,
+                "attention_scatter: text_row0 must equal rows_per_rank * nranks");
+  attn::OutMap om{};
+  om.ldo = ldo, om.o_head_stride = o_head_stride, om.nranks = nranks;
+  om.rows_per_rank = rows_per_rank, om.text_row0 = text_row0;
+  for (int r = 0; r < nranks; ++r) {
+    AQB_CHECK_ARG(peer_o[r] && reinterpret_cast<uintptr_t>(peer_o[r]) % 16 == 0, "attention_scatter: peer_o[%d]", r);
+    om.peer_o[r] = reinterpret_cast<__nv_bfloat16*>(peer_o[r]);
+  }
+  return attn::run(q, ldq, q_head_stride, k, ldk, k_head_stride, v, ldv, v_head_stride, seq_q, seq_kv, heads,
+                   head_dim, softmax_scale, kv_splits, workspace, workspace_bytes, om, run_flag, run_if,
+                   reinterpret_cast<cudaStream_t>(stream));
 }

@@ -29,10 +29,22 @@ AQB_DEV float4 ld_stream(const float4* p) {
 
 // ------------------------------------------------------------ norm+modulate
 // One warp per row; NV float4 per lane (hidden = 128 * NV).
-template <int NV>
+AQB_DEV void store4(__nv_bfloat16* p, float4 o) {
+  *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
+}
+AQB_DEV void store4(float* p, float4 o) { *reinterpret_cast<float4*>(p) = o; }
+AQB_DEV float2 load2(const __nv_bfloat16* p) { return __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(p)); }
+AQB_DEV float2 load2(const float* p) { return *reinterpret_cast<const float2*>(p); }
+AQB_DEV void store2(__nv_bfloat16* p, float2 v) {
+  *reinterpret_cast<__nv_bfloat162*>(p) = __floats2bfloat162_rn(v.x, v.y);
+}
+AQB_DEV void store2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
+
+// OutT = bf16 (product path) or float (fp32 validation mode).
+template <int NV, typename OutT>
 __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__ x, int64_t ldx,
                                                        const float* __restrict__ shift,
-                                                       const float* __restrict__ scale, __nv_bfloat16* __restrict__ y,
+                                                       const float* __restrict__ scale, OutT* __restrict__ y,
                                                        int64_t ldy, int64_t rows, float eps, int kind,
                                                        float* __restrict__ prev, float* __restrict__ partials,
                                                        const int32_t* flag, int32_t run_if) {
@@ -64,7 +76,7 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
   }
   const float4* sh4 = reinterpret_cast<const float4*>(shift);
   const float4* sc4 = reinterpret_cast<const float4*>(scale);
-  __nv_bfloat16* yr = y + row * ldy;
+  OutT* yr = y + row * ldy;
   float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
   float dsum = 0.f, psum = 0.f;
 #pragma unroll
@@ -77,7 +89,7 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
     o.y = (v[j].y - mean) * rstd * (1.f + sc.y) + sh.y;
     o.z = (v[j].z - mean) * rstd * (1.f + sc.z) + sh.z;
     o.w = (v[j].w - mean) * rstd * (1.f + sc.w) + sh.w;
-    *reinterpret_cast<uint2*>(yr + 4 * c4) = make_uint2(pack_bf16(o.x, o.y), pack_bf16(o.z, o.w));
+    store4(yr + 4 * c4, o);
     if (pr) {
       const float4 p = pr[c4];
       dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
@@ -97,11 +109,11 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
 
 // ------------------------------------------------------- QK-norm + 3D RoPE
 // One warp per (row, head); lane handles pairs lane, lane+32, ... (D/2 pairs).
-template <int D>
+template <int D, typename T>
 __global__ void __launch_bounds__(256) qk_norm_rope_kernel(
-    const __nv_bfloat16* __restrict__ src, int64_t ld_src, int64_t rows, int heads, int head_begin, int head_count,
+    const T* __restrict__ src, int64_t ld_src, int64_t rows, int heads, int head_begin, int head_count,
     const float* __restrict__ qw, const float* __restrict__ kw, float eps, const float* __restrict__ rcos,
-    const float* __restrict__ rsin, int64_t rope_row0, int64_t rope_rows, __nv_bfloat16* dst, int64_t g_stride,
+    const float* __restrict__ rsin, int64_t rope_row0, int64_t rope_rows, T* dst, int64_t g_stride,
     int64_t r_stride, int64_t w_stride, int hpg, int parts, int norm_parts, const int32_t* flag, int32_t run_if) {
   if (!gate_open(flag, run_if)) return;
   constexpr int NP = (D / 2 + 31) / 32;  // pairs per lane
@@ -111,20 +123,19 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(
   const int64_t r = item / head_count;
   const int j = static_cast<int>(item - r * head_count);
   const int h = head_begin + j;
-  const __nv_bfloat16* s = src + r * ld_src;
-  __nv_bfloat16* d = dst + static_cast<int64_t>(j / hpg) * g_stride + r * r_stride + static_cast<int64_t>(j % hpg) * D;
+  const T* s = src + r * ld_src;
+  T* d = dst + static_cast<int64_t>(j / hpg) * g_stride + r * r_stride + static_cast<int64_t>(j % hpg) * D;
   const int64_t grow = rope_row0 + r;
   const bool rope = grow < rope_rows;
 #pragma unroll 1
   for (int which = 0; which < parts; ++which) {
-    const __nv_bfloat162* sp =
-        reinterpret_cast<const __nv_bfloat162*>(s + static_cast<int64_t>(which) * heads * D + static_cast<int64_t>(h) * D);
+    const T* sp = s + static_cast<int64_t>(which) * heads * D + static_cast<int64_t>(h) * D;
     float2 e[NP];
     float ss = 0.f;
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
       const int p = lane + 32 * i;
-      e[i] = (p < D / 2) ? __bfloat1622float2(sp[p]) : make_float2(0.f, 0.f);
+      e[i] = (p < D / 2) ? load2(sp + 2 * p) : make_float2(0.f, 0.f);
       ss += e[i].x * e[i].x + e[i].y * e[i].y;
     }
     if (which < norm_parts) {
@@ -146,11 +157,11 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(
         }
       }
     }
-    __nv_bfloat162* dp = reinterpret_cast<__nv_bfloat162*>(d + static_cast<int64_t>(which) * w_stride);
+    T* dp = d + static_cast<int64_t>(which) * w_stride;
 #pragma unroll
     for (int i = 0; i < NP; ++i) {
       const int p = lane + 32 * i;
-      if (p < D / 2) dp[p] = __floats2bfloat162_rn(e[i].x, e[i].y);
+      if (p < D / 2) store2(dp + 2 * p, e[i]);
     }
   }
 }
@@ -344,10 +355,10 @@ static int grid_for(int64_t n, int threads) {
 
 using namespace aqb;
 
-extern "C" int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* y,
-                                 int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
-                                 float* probe_prev, float* probe_partials, const int32_t* run_flag, int32_t run_if,
-                                 void* stream) {
+template <typename OutT>
+static int norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* y, int64_t ldy,
+                         int64_t rows, int32_t hidden, float eps, int32_t norm_kind, float* probe_prev,
+                         float* probe_partials, const int32_t* run_flag, int32_t run_if, void* stream) {
   AQB_CHECK_ARG(x && y, "norm_modulate: null pointer");
   AQB_CHECK_ARG(hidden % 128 == 0 && hidden >= 128 && hidden <= 4096, "norm_modulate: hidden %d unsupported", hidden);
   AQB_CHECK_ARG(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= hidden && ldy >= hidden, "norm_modulate: bad strides");
@@ -356,11 +367,11 @@ extern "C" int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift
   if (rows <= 0) return AQB_OK;
   const int grid = static_cast<int>((rows + 7) / 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  __nv_bfloat16* yb = reinterpret_cast<__nv_bfloat16*>(y);
+  OutT* yb = reinterpret_cast<OutT*>(y);
 #define NM_CASE(NV)                                                                                          \
   case NV:                                                                                                   \
-    norm_mod_kernel<NV><<<grid, 256, 0, s>>>(x, ldx, shift, scale, yb, ldy, rows, eps, norm_kind, probe_prev, \
-                                             probe_partials, run_flag, run_if);                              \
+    norm_mod_kernel<NV, OutT><<<grid, 256, 0, s>>>(x, ldx, shift, scale, yb, ldy, rows, eps, norm_kind,      \
+                                                   probe_prev, probe_partials, run_flag, run_if);            \
     break;
   switch (hidden / 128) {
     NM_CASE(1) NM_CASE(2) NM_CASE(3) NM_CASE(4) NM_CASE(6) NM_CASE(8) NM_CASE(12) NM_CASE(16) NM_CASE(20)
@@ -373,12 +384,28 @@ extern "C" int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift
   return AQB_OK;
 }
 
-extern "C" int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t heads, int32_t head_begin,
-                                int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
-                                const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows,
-                                void* dst, int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride,
-                                int32_t hpg, int32_t parts, int32_t norm_parts, const int32_t* run_flag,
-                                int32_t run_if, void* stream) {
+extern "C" int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* y,
+                                 int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
+                                 float* probe_prev, float* probe_partials, const int32_t* run_flag, int32_t run_if,
+                                 void* stream) {
+  return norm_modulate<__nv_bfloat16>(x, ldx, shift, scale, y, ldy, rows, hidden, eps, norm_kind, probe_prev,
+                                      probe_partials, run_flag, run_if, stream);
+}
+
+extern "C" int aqb_norm_modulate_f32(const float* x, int64_t ldx, const float* shift, const float* scale, float* y,
+                                     int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
+                                     float* probe_prev, float* probe_partials, const int32_t* run_flag,
+                                     int32_t run_if, void* stream) {
+  return norm_modulate<float>(x, ldx, shift, scale, y, ldy, rows, hidden, eps, norm_kind, probe_prev,
+                              probe_partials, run_flag, run_if, stream);
+}
+
+template <typename T>
+static int qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t heads, int32_t head_begin,
+                        int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
+                        const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows, void* dst,
+                        int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride, int32_t hpg,
+                        int32_t parts, int32_t norm_parts, const int32_t* run_flag, int32_t run_if, void* stream) {
   AQB_CHECK_ARG(src && dst, "qk_norm_rope: null pointer");
   AQB_CHECK_ARG(parts >= 1 && parts <= 3 && norm_parts >= 0 && norm_parts <= parts && norm_parts <= 2,
                 "qk_norm_rope: bad parts");
@@ -392,14 +419,14 @@ extern "C" int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, i
   const int64_t items = rows * head_count;
   const int grid = static_cast<int>((items + 7) / 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  auto sp = reinterpret_cast<const __nv_bfloat16*>(src);
-  auto dp = reinterpret_cast<__nv_bfloat16*>(dst);
+  auto sp = reinterpret_cast<const T*>(src);
+  auto dp = reinterpret_cast<T*>(dst);
 #define QK_CASE(D)                                                                                                \
   case D:                                                                                                         \
-    qk_norm_rope_kernel<D><<<grid, 256, 0, s>>>(sp, ld_src, rows, heads, head_begin, head_count, q_w, k_w, eps,   \
-                                                rope_cos, rope_sin, rope_row0, rope_rows, dp, dst_group_stride,   \
-                                                dst_row_stride, dst_which_stride, hpg, parts, norm_parts, run_flag,    \
-                                                run_if);                                                          \
+    qk_norm_rope_kernel<D, T><<<grid, 256, 0, s>>>(sp, ld_src, rows, heads, head_begin, head_count, q_w, k_w,     \
+                                                   eps, rope_cos, rope_sin, rope_row0, rope_rows, dp,             \
+                                                   dst_group_stride, dst_row_stride, dst_which_stride, hpg, parts, \
+                                                   norm_parts, run_flag, run_if);                                 \
     break;
   switch (head_dim) {
     QK_CASE(32) QK_CASE(64) QK_CASE(128) QK_CASE(256)
@@ -409,6 +436,28 @@ extern "C" int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, i
 #undef QK_CASE
   AQB_LAUNCH_CHECK();
   return AQB_OK;
+}
+
+extern "C" int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t heads, int32_t head_begin,
+                                int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w, float eps,
+                                const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows,
+                                void* dst, int64_t dst_group_stride, int64_t dst_row_stride, int64_t dst_which_stride,
+                                int32_t hpg, int32_t parts, int32_t norm_parts, const int32_t* run_flag,
+                                int32_t run_if, void* stream) {
+  return qk_norm_rope<__nv_bfloat16>(src, ld_src, rows, heads, head_begin, head_count, head_dim, q_w, k_w, eps,
+                                     rope_cos, rope_sin, rope_row0, rope_rows, dst, dst_group_stride, dst_row_stride,
+                                     dst_which_stride, hpg, parts, norm_parts, run_flag, run_if, stream);
+}
+
+extern "C" int aqb_qk_norm_rope_f32(const float* src, int64_t ld_src, int64_t rows, int32_t heads, int32_t head_begin,
+                                    int32_t head_count, int32_t head_dim, const float* q_w, const float* k_w,
+                                    float eps, const float* rope_cos, const float* rope_sin, int64_t rope_row0,
+                                    int64_t rope_rows, float* dst, int64_t dst_group_stride, int64_t dst_row_stride,
+                                    int64_t dst_which_stride, int32_t hpg, int32_t parts, int32_t norm_parts,
+                                    const int32_t* run_flag, int32_t run_if, void* stream) {
+  return qk_norm_rope<float>(src, ld_src, rows, heads, head_begin, head_count, head_dim, q_w, k_w, eps, rope_cos,
+                             rope_sin, rope_row0, rope_rows, dst, dst_group_stride, dst_row_stride, dst_which_stride,
+                             hpg, parts, norm_parts, run_flag, run_if, stream);
 }
 
 extern "C" int aqb_gemv(const void* w, const float* x, const float* t, const float* b, const float* add, float* y,

@@ -62,7 +62,15 @@ struct Params {
   int part_width;         // heads * 128
   int norm_parts;         // parts < norm_parts are RMS-normed (+ RoPE)
   int hpg, g_base, groups;  // heads per output group (Ulysses), group offset, group count
+  int peer_groups;          // 1: group g is TMA-stored through PeerMaps::m[g] (another rank's buffer)
   float eps;
+};
+
+// Per-destination-rank output maps of the Ulysses scatter (QK-norm epilogue):
+// map g addresses this rank's row block inside rank g's attention-input buffer.
+constexpr int kMaxPeers = 8;
+struct PeerMaps {
+  CUtensorMap m[kMaxPeers];
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int& nb) {
@@ -148,8 +156,8 @@ __device__ __forceinline__ void epilogue_prologue(const Params& p, const CUtenso
 
 // One accumulator tile (this CTA's 128 rows x BN columns starting at col_base).
 template <int EPI, int BN>
-__device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmo, EpiState& es, uint32_t tacc,
-                                              int row0, int col_base, uint32_t q, uint32_t lane) {
+__device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmo, const PeerMaps* pm, EpiState& es,
+                                              uint32_t tacc, int row0, int col_base, uint32_t q, uint32_t lane) {
   const int r = q * 32 + lane;           // row within the CTA tile (= TMEM lane)
   const uint32_t lane_off = (q * 32) << 16;
   const bool leader_thread = (q == 0 && lane == 0);
@@ -240,7 +248,10 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
         fence_proxy_async_smem();
         named_bar_sync(1, 128);
         if (leader_thread) {
-          tma_store_5d(tmo, buf, 64 * half, head % p.hpg, part, row0, grp);
+          if (p.peer_groups)
+            tma_store_5d(&pm->m[grp], buf, 64 * half, head % p.hpg, part, row0, 0);
+          else
+            tma_store_5d(tmo, buf, 64 * half, head % p.hpg, part, row0, grp);
           bulk_commit();
         }
         ++es.chunk;
@@ -338,7 +349,7 @@ constexpr int smem_bytes() {
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                const __grid_constant__ CUtensorMap tma_o, Params p) {
+                const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ PeerMaps pm, Params p) {
   if (!gate_open(p.run_flag, p.run_if)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -432,7 +443,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       epilogue_prologue<EPI>(p, &tma_o, es, mb * BM, nb * BN, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      epilogue_tile<EPI, BN>(p, &tma_o, es, tmem + acc * BN, mb * BM, nb * BN, q, lane);
+      epilogue_tile<EPI, BN>(p, &tma_o, &pm, es, tmem + acc * BN, mb * BM, nb * BN, q, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
@@ -452,7 +463,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 template <int BN, int STAGES, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                 const __grid_constant__ CUtensorMap tma_o, Params p) {
+                 const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ PeerMaps pm, Params p) {
   if (!gate_open(p.run_flag, p.run_if)) return;
   constexpr int BNH = BN / 2;  // W rows per CTA
   constexpr int kABytes = BM * BK * 2, kBBytes = BNH * BK * 2;
@@ -554,7 +565,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       epilogue_prologue<EPI>(p, &tma_o, es, mb * (2 * BM) + rank * BM, nb * BN, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      epilogue_tile<EPI, BN>(p, &tma_o, es, tmem + acc * BN, mb * (2 * BM) + rank * BM, nb * BN, q, lane);
+      epilogue_tile<EPI, BN>(p, &tma_o, &pm, es, tmem + acc * BN, mb * (2 * BM) + rank * BM, nb * BN, q, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -577,7 +588,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 }
 
 template <int BN, int STAGES, int EPI, bool PAIR>
-int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const Params& p, cudaStream_t stream) {
+int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const PeerMaps& pm, const Params& p,
+           cudaStream_t stream) {
   constexpr int smem = smem_bytes<BN, STAGES, PAIR, EPI>();
   static_assert(smem <= 232448, "shared memory budget");
   auto kern = PAIR ? gemm2_kernel<BN, STAGES, EPI> : gemm_kernel<BN, STAGES, EPI>;
@@ -593,23 +605,23 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, 
   } else {
     grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
   }
-  kern<<<grid, kThreads, smem, stream>>>(ta, tb, to, p);
+  kern<<<grid, kThreads, smem, stream>>>(ta, tb, to, pm, p);
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
 
 template <int BN, int STAGES, bool PAIR>
-int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const Params& p,
-                 cudaStream_t s) {
+int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const PeerMaps& pm,
+                 const Params& p, cudaStream_t s) {
   // one pipeline stage makes room for the third gate*residual buffer
   constexpr int kResStages = STAGES - ((PAIR ? BM + BN / 2 : BM + BN) * BK * 2 >= kEpiBuf * 2 ? 1 : 1);
   switch (epi) {
-    case AQB_EPI_BF16: return launch<BN, STAGES, AQB_EPI_BF16, PAIR>(ta, tb, to, p, s);
-    case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16, PAIR>(ta, tb, to, p, s);
-    case AQB_EPI_GATE_RES: return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, p, s);
-    case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32, PAIR>(ta, tb, to, p, s);
-    case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER, PAIR>(ta, tb, to, p, s);
-    case AQB_EPI_QKNORM_ROPE: return launch<BN, STAGES, AQB_EPI_QKNORM_ROPE, PAIR>(ta, tb, to, p, s);
+    case AQB_EPI_BF16: return launch<BN, STAGES, AQB_EPI_BF16, PAIR>(ta, tb, to, pm, p, s);
+    case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16, PAIR>(ta, tb, to, pm, p, s);
+    case AQB_EPI_GATE_RES: return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, pm, p, s);
+    case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32, PAIR>(ta, tb, to, pm, p, s);
+    case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER, PAIR>(ta, tb, to, pm, p, s);
+    case AQB_EPI_QKNORM_ROPE: return launch<BN, STAGES, AQB_EPI_QKNORM_ROPE, PAIR>(ta, tb, to, pm, p, s);
   }
   return set_error(AQB_EINVAL, "unknown epilogue %d", epi);
 }
@@ -658,7 +670,9 @@ namespace gemm {
 
 // Shared host path: A/W tensor maps, variant choice, tile bookkeeping, launch.
 static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n, int64_t k, int epilogue,
-               Params& p, const CUtensorMap& to, int variant, cudaStream_t s) {
+               Params& p, const CUtensorMap& to, int variant, cudaStream_t s, const PeerMaps* pm_in = nullptr) {
+  static const PeerMaps kNoPeers{};
+  const PeerMaps& pm = pm_in ? *pm_in : kNoPeers;
   const bool pair = variant == V2_256 || variant == V2_128;
   const int bn = (variant == V1_256 || variant == V2_256) ? 256 : 128;
   const int tile_m = pair ? 2 * BM : BM;
@@ -683,10 +697,10 @@ static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m
   p.num_tiles = p.num_m * p.num_n;
   p.group_m = 16;
   switch (variant) {
-    case V1_256: return dispatch_epi<256, 4, false>(epilogue, ta, tb, to, p, s);
-    case V1_128: return dispatch_epi<128, 6, false>(epilogue, ta, tb, to, p, s);
-    case V2_256: return dispatch_epi<256, 6, true>(epilogue, ta, tb, to, p, s);
-    default: return dispatch_epi<128, 8, true>(epilogue, ta, tb, to, p, s);
+    case V1_256: return dispatch_epi<256, 4, false>(epilogue, ta, tb, to, pm, p, s);
+    case V1_128: return dispatch_epi<128, 6, false>(epilogue, ta, tb, to, pm, p, s);
+    case V2_256: return dispatch_epi<256, 6, true>(epilogue, ta, tb, to, pm, p, s);
+    default: return dispatch_epi<128, 8, true>(epilogue, ta, tb, to, pm, p, s);
   }
 }
 
@@ -731,15 +745,16 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
   return run(a, lda, w, ldw, m, n, k, epilogue, p, to, variant, reinterpret_cast<cudaStream_t>(stream));
 }
 
-extern "C" int aqb_gemm_qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n,
-                                    int64_t k, const float* bias, int32_t part_width, int32_t norm_parts,
-                                    const float* q_w, const float* k_w, float eps, const float* rope_cos,
-                                    const float* rope_sin, int64_t rope_row0, int64_t rope_rows, void* out,
-                                    int64_t out_row_stride, int32_t groups, int64_t group_stride, int32_t hpg,
-                                    int32_t g_base, const int32_t* run_flag, int32_t run_if, void* stream) {
-  using namespace aqb;
-  using namespace aqb::gemm;
-  AQB_CHECK_ARG(a && w && out, "gemm_qknorm_rope: null pointer");
+namespace aqb {
+namespace gemm {
+
+static int qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n, int64_t k,
+                       const float* bias, int32_t part_width, int32_t norm_parts, const float* q_w, const float* k_w,
+                       float eps, const float* rope_cos, const float* rope_sin, int64_t rope_row0, int64_t rope_rows,
+                       void* out, int64_t out_row_stride, int32_t groups, int64_t group_stride, int32_t hpg,
+                       int32_t g_base, void* const* peer_out, const int32_t* run_flag, int32_t run_if,
+                       cudaStream_t stream) {
+  AQB_CHECK_ARG(a && w && (out || peer_out), "gemm_qknorm_rope: null pointer");
   AQB_CHECK_ARG(m >= 1 && k >= 1 && k % 8 == 0 && lda % 8 == 0 && ldw % 8 == 0, "gemm_qknorm_rope: bad shape");
   AQB_CHECK_ARG(part_width >= 128 && part_width % 128 == 0 && n % part_width == 0 && n / part_width <= 3,
                 "gemm_qknorm_rope: columns must be [parts<=3][heads][128]");
@@ -750,14 +765,26 @@ extern "C" int aqb_gemm_qknorm_rope(const void* a, int64_t lda, const void* w, i
   AQB_CHECK_ARG(hpg >= 1 && groups >= 1 && out_row_stride % 8 == 0 && group_stride % 8 == 0,
                 "gemm_qknorm_rope: bad output layout");
   const int parts = int(n / part_width);
+  // (d:128, head-in-group:hpg, part, row:m, group) ; strides in bytes
+  const uint64_t strides[4] = {256, uint64_t(hpg) * 256, uint64_t(out_row_stride) * 2, uint64_t(group_stride) * 2};
+  const uint32_t box[5] = {64, 1, 1, uint32_t(BM), 1};
   CUtensorMap to;
-  {
-    // (d:128, head-in-group:hpg, part, row:m, group) ; strides in bytes
-    uint64_t dims[5] = {128, uint64_t(hpg), uint64_t(parts), uint64_t(m), uint64_t(groups)};
-    uint64_t strides[4] = {256, uint64_t(hpg) * 256, uint64_t(out_row_stride) * 2, uint64_t(group_stride) * 2};
-    uint32_t box[5] = {64, 1, 1, uint32_t(BM), 1};
+  PeerMaps pm;
+  memset(&pm, 0, sizeof(pm));
+  if (peer_out == nullptr) {
+    const uint64_t dims[5] = {128, uint64_t(hpg), uint64_t(parts), uint64_t(m), uint64_t(groups)};
     int rc = make_tmap(&to, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, out, 5, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
+  } else {
+    AQB_CHECK_ARG(groups <= kMaxPeers && g_base == 0, "gemm_qknorm_rope_scatter: 1..%d ranks", kMaxPeers);
+    const uint64_t dims[5] = {128, uint64_t(hpg), uint64_t(parts), uint64_t(m), 1};
+    for (int g = 0; g < groups; ++g) {
+      AQB_CHECK_ARG(peer_out[g] != nullptr, "gemm_qknorm_rope_scatter: peer_out[%d] is null", g);
+      int rc = make_tmap(&pm.m[g], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, peer_out[g], 5, dims, strides, box,
+                         CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rc) return rc;
+    }
+    to = pm.m[0];
   }
   Params p{};
   p.out = out, p.ldo = out_row_stride, p.bias = bias;
@@ -765,6 +792,34 @@ extern "C" int aqb_gemm_qknorm_rope(const void* a, int64_t lda, const void* w, i
   p.norm_w0 = q_w, p.norm_w1 = k_w, p.rope_cos = rope_cos, p.rope_sin = rope_sin;
   p.rope_row0 = rope_row0, p.rope_rows = rope_rows, p.part_width = part_width, p.norm_parts = norm_parts;
   p.hpg = hpg, p.g_base = g_base, p.groups = groups, p.eps = eps;
-  return run(a, lda, w, ldw, m, n, k, AQB_EPI_QKNORM_ROPE, p, to, pick_variant(m, n, k),
-             reinterpret_cast<cudaStream_t>(stream));
+  p.peer_groups = peer_out != nullptr;
+  return run(a, lda, w, ldw, m, n, k, AQB_EPI_QKNORM_ROPE, p, to, pick_variant(m, n, k), stream,
+             peer_out ? &pm : nullptr);
+}
+
+}  // namespace gemm
+}  // namespace aqb
+
+extern "C" int aqb_gemm_qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n,
+                                    int64_t k, const float* bias, int32_t part_width, int32_t norm_parts,
+                                    const float* q_w, const float* k_w, float eps, const float* rope_cos,
+                                    const float* rope_sin, int64_t rope_row0, int64_t rope_rows, void* out,
+                                    int64_t out_row_stride, int32_t groups, int64_t group_stride, int32_t hpg,
+                                    int32_t g_base, const int32_t* run_flag, int32_t run_if, void* stream) {
+  return aqb::gemm::qknorm_rope(a, lda, w, ldw, m, n, k, bias, part_width, norm_parts, q_w, k_w, eps, rope_cos,
+                                rope_sin, rope_row0, rope_rows, out, out_row_stride, groups, group_stride, hpg, g_base,
+                                nullptr, run_flag, run_if, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int aqb_gemm_qknorm_rope_scatter(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m,
+                                            int64_t n, int64_t k, const float* bias, int32_t part_width,
+                                            int32_t norm_parts, const float* q_w, const float* k_w, float eps,
+                                            const float* rope_cos, const float* rope_sin, int64_t rope_row0,
+                                            int64_t rope_rows, void* const* peer_out, int32_t nranks,
+                                            int64_t out_row_stride, int32_t hpg, const int32_t* run_flag,
+                                            int32_t run_if, void* stream) {
+  AQB_CHECK_ARG(peer_out != nullptr && nranks >= 1, "gemm_qknorm_rope_scatter: peer_out");
+  return aqb::gemm::qknorm_rope(a, lda, w, ldw, m, n, k, bias, part_width, norm_parts, q_w, k_w, eps, rope_cos,
+                                rope_sin, rope_row0, rope_rows, nullptr, out_row_stride, nranks, 0, hpg, 0, peer_out,
+                                run_flag, run_if, reinterpret_cast<cudaStream_t>(stream));
 }

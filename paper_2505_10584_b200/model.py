@@ -37,11 +37,12 @@ import torch
 from . import ops
 from .config import DiTConfig
 from .errors import ConfigError
-from .parallel import Ulysses
+from .parallel import SIGNAL_BYTES, PeerBuffers, Ulysses
 from .schedule import front_block_count
 from .weights import init_weights
 
 BF16, F32 = torch.bfloat16, torch.float32
+PRECISIONS = ("bf16", "fp32")
 
 
 def rope_tables(grid, dims, theta, device):
@@ -75,9 +76,18 @@ class DiTModel:
     """Executable DiT (either family) bound to one GPU / one Ulysses rank."""
 
     def __init__(self, cfg: DiTConfig, weights: dict | None = None, seed: int = 0, device="cuda",
-                 sp: Ulysses | None = None, cached_cost_fraction: float = 0.25):
+                 sp: Ulysses | None = None, cached_cost_fraction: float = 0.25, precision: str = "bf16"):
+        """``precision``: ``"bf16"`` (the product path: bf16 activations, tcgen05 kernels) or
+        ``"fp32"`` (validation mode, north_star <= 1e-4: fp32 activations, SIMT kernels; 1 GPU)."""
         if not torch.cuda.is_available():
             raise ConfigError("a CUDA device is required (no CPU fallback)", "device")
+        if precision not in PRECISIONS:
+            raise ConfigError(f"precision must be one of {PRECISIONS}", "model.precision")
+        if precision == "fp32" and sp is not None and sp.P > 1:
+            raise ConfigError("fp32 validation mode runs on one GPU", "model.precision")
+        self.precision = precision
+        self.fp32 = precision == "fp32"
+        self.act = F32 if self.fp32 else BF16
         self.cfg = cfg
         self.device = torch.device(device)
         self.sp = sp
@@ -124,7 +134,7 @@ class DiTModel:
         self.geo = _Geometry(grid, Sv, Sv_loc, St, Sv_loc + St)
         H, F, A, D = cfg.hidden_size, cfg.ffn_dim, cfg.num_heads, cfg.head_dim
         rows = self.geo.rows
-        e = lambda *s, dt=BF16: torch.empty(*s, device=dev, dtype=dt)  # noqa: E731
+        e = lambda *s, dt=self.act: torch.empty(*s, device=dev, dtype=dt)  # noqa: E731
         self.x = e(rows, H, dt=F32)
         self.m = e(rows, H)
         self.qkv = e(rows, 3 * H)
@@ -143,7 +153,7 @@ class DiTModel:
         self.sums = e(2, dt=F32)
         self.cstate = torch.zeros(4, device=dev, dtype=torch.int32)
         self.flag = self.cstate[1:2]
-        t_bf = text.to(dev, F32).to(BF16).contiguous()
+        t_bf = text.to(dev, F32).to(self.act).contiguous()
         W = self.W
         if cfg.family == "single-dit":
             self.t0 = e(H, dt=F32)
@@ -171,16 +181,45 @@ class DiTModel:
             self.allmods = e(self.mod_w.shape[0], dt=F32)
             self.txt0 = e(St, H, dt=F32)
             ops.gemm(t_bf, W["txt_in.w"], self.txt0, bias=W["txt_in.b"], epilogue="f32")
-        if self.sp is not None and self.sp.P > 1:
-            hl = A // P
-            self.hl = hl
-            self.a2a_snd = e(P, Sv_loc, 3, hl, D)
-            self.a2a_rcv = e(Sv + St, 3, hl, D)
-            self.oh = e(Sv + St, hl * D)
-            self.ob = e(P, Sv_loc, hl * D)
-            if St:
-                self.tg = e(P, St, hl * D)
+        self.peer = None
+        hl = A // P
+        self.hl = hl
+        if self.sp is not None and P > 1:
+            if self.sp.exchange == "p2p" and D == 128:
+                # symmetric buffers: attention input (all heads of this rank's group, full
+                # sequence) and the residual-row-major attention output
+                rs = 3 * hl * D
+                self.peer = PeerBuffers(self.sp, {"rcv": (Sv + St) * rs * 2, "o": rows * H * 2,
+                                                  "sig": SIGNAL_BYTES}, dev)
+                self.a2a_rcv = self.peer.local("rcv", (Sv + St, 3, hl, D), BF16)
+                self.o = self.peer.local("o", (rows, H), BF16)
+                r = self.sp.rank
+                self.qkv_dst = self.peer.ptrs("rcv", r * Sv_loc * rs * 2)
+                self.o_dst = self.peer.ptrs("o", r * hl * D * 2)
+                self.sig = self.peer.ptrs("sig")
+                self.epoch = torch.zeros(1, device=dev, dtype=torch.int32)
+                self.peer_status = torch.zeros(1, device=dev, dtype=torch.int32)
+            else:
+                self.a2a_snd = e(P, Sv_loc, 3, hl, D)
+                self.a2a_rcv = e(Sv + St, 3, hl, D)
+                self.oh = e(Sv + St, hl * D)
+                self.ob = e(P, Sv_loc, hl * D)
+                if St:
+                    self.tg = e(P, St, hl * D)
+        # split-KV workspace for the attention launches of this geometry
+        need = ops.attention_workspace_bytes(Sv + St if P > 1 else rows, Sv + St, hl, D)
+        if cfg.family == "single-dit":
+            need = max(need, ops.attention_workspace_bytes(Sv_loc, cfg.text_len, A, D))
+        self.attn_ws = torch.empty(max(need, 16), device=dev, dtype=torch.uint8)
         return self
+
+    def _barrier(self, flag=None, run_if=1, payload=None):
+        ops.peer_barrier(self.sig, self.sp.rank, self.epoch, self.peer_status, payload=payload,
+                         pay_out=payload, run_flag=flag, run_if=run_if)
+
+    def peer_ok(self) -> bool:
+        """False if a peer barrier timed out (a rank never arrived) since prepare()."""
+        return self.peer is None or int(self.peer_status.item()) == 0
 
     # ------------------------------------------------------------- primitives
     def _mod(self, name):
@@ -208,7 +247,7 @@ class DiTModel:
         cfg, g, W = self.cfg, self.geo, self.W
         A, D, H, eps = cfg.num_heads, cfg.head_dim, cfg.hidden_size, cfg.qk_norm_eps
         n, R, St = g.Sv_loc, g.rows, g.St
-        fused = D == 128
+        fused = D == 128 and not self.fp32
         m, qkv = self.m, self.qkv
         wi, bi = W[f"{pi}.qkv.w"], W[f"{pi}.qkv.b"]
         if pt is not None:
@@ -234,11 +273,28 @@ class DiTModel:
                 if St:
                     ops.qk_norm_rope(qkv[n:], A, D, W[f"{pt}.q_norm"], W[f"{pt}.k_norm"], eps, run_flag=flag,
                                      run_if=run_if)
-            ops.attention(qkv, qkv[:, H:], qkv[:, 2 * H:], self.o, A, D, run_flag=flag, run_if=run_if)
+            ops.attention(qkv, qkv[:, H:], qkv[:, 2 * H:], self.o, A, D, workspace=self.attn_ws, run_flag=flag,
+                          run_if=run_if)
             return
         sp, P, hl = self.sp, self.sp.P, self.hl
-        snd, rcv = self.a2a_snd, self.a2a_rcv
+        rcv = self.a2a_rcv
         rs = 3 * hl * D  # row stride of the packed layouts
+        if self.peer is not None:
+            # fused exchange: QKV epilogue -> owners' input buffers, attention epilogue -> owners' O rows
+            ops.gemm_qknorm_rope_scatter(m[:n], wi, self.qkv_dst, H, 2, W[f"{pi}.q_norm"], W[f"{pi}.k_norm"], eps, rs,
+                                         hl, bias=bi, cos=self.cos, sin=self.sin, rope_row0=sp.rank * n,
+                                         rope_rows=g.Sv, run_flag=flag, run_if=run_if)
+            if St:
+                ops.gemm_qknorm_rope(m[n:], wt, rcv[g.Sv:].view(St, -1), H, 2, W[f"{pt}.q_norm"], W[f"{pt}.k_norm"],
+                                     eps, bias=bt, out_row_stride=rs, groups=1, hpg=hl, g_base=sp.rank,
+                                     run_flag=flag, run_if=run_if)
+            self._barrier(flag, run_if)
+            q = rcv.view(g.Sv + St, -1)
+            ops.attention_scatter(q, q[:, hl * D:], q[:, 2 * hl * D:], self.o_dst, H, hl, D, n, g.Sv,
+                                  workspace=self.attn_ws, run_flag=flag, run_if=run_if)
+            self._barrier(flag, run_if)
+            return
+        snd = self.a2a_snd
         if fused:
             ops.gemm_qknorm_rope(m[:n], wi, snd, H, 2, W[f"{pi}.q_norm"], W[f"{pi}.k_norm"], eps, bias=bi,
                                  cos=self.cos, sin=self.sin, rope_row0=sp.rank * n, rope_rows=g.Sv, out_row_stride=rs,
@@ -261,7 +317,8 @@ class DiTModel:
                                  head_begin=sp.rank * hl, head_count=hl, hpg=hl, dst_row_stride=rs,
                                  dst_which_stride=hl * D, run_flag=flag, run_if=run_if)
         q = rcv.view(g.Sv + St, -1)
-        ops.attention(q, q[:, hl * D:], q[:, 2 * hl * D:], self.oh, hl, D, run_flag=flag, run_if=run_if)
+        ops.attention(q, q[:, hl * D:], q[:, 2 * hl * D:], self.oh, hl, D, workspace=self.attn_ws, run_flag=flag,
+                      run_if=run_if)
         sp.all_to_all(self.ob.view(-1), self.oh[:g.Sv].reshape(-1))
         ops.heads_to_seq(self.ob, n, P, hl * D, self.o[:n], run_flag=flag, run_if=run_if)
         if St:
@@ -297,7 +354,7 @@ class DiTModel:
         ops.qk_norm_rope(self.xq, A, D, W[f"{p}.xq_norm"], None, cfg.qk_norm_eps, parts=1, norm_parts=1,
                          run_flag=flag, run_if=run_if)
         kv = self.text_kv[i]
-        ops.attention(self.xq, kv, kv[:, H:], self.o, A, D, run_flag=flag, run_if=run_if)
+        ops.attention(self.xq, kv, kv[:, H:], self.o, A, D, workspace=self.attn_ws, run_flag=flag, run_if=run_if)
         ops.gemm(self.o, W[f"{p}.xproj.w"], self.x, bias=W[f"{p}.xproj.b"], epilogue="gate_res", run_flag=flag,
                  run_if=run_if)
         self._mlp(p, 0, n, mods, flag, run_if)
@@ -384,7 +441,9 @@ class DiTModel:
     def _decide(self):
         pol = self.policy
         ops.rel_l1_reduce(self.partials, self.geo.Sv_loc, self.sums)
-        if self.sp is not None and self.sp.P > 1:
+        if self.peer is not None:
+            self._barrier(payload=self.sums)  # sums over ranks, rank order, identical everywhere
+        elif self.sp is not None and self.sp.P > 1:
             self.sp.all_reduce_sum(self.sums)
         ops.cache_decide(self.sums, self.cstate, pol.threshold, pol.warmup, self.num_steps, pol.force_last,
                          self.flags_out, self.rels_out)

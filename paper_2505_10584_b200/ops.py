@@ -87,31 +87,36 @@ def _need(t, dtype, name):
 
 def norm_modulate(x, shift, scale, out, eps=1e-6, kind=0, probe_prev=None, probe_partials=None,
                   run_flag=None, run_if=1):
-    """out[bf16] = norm(x)·(1+scale)+shift, row-wise over the last dim."""
+    """out = norm(x)·(1+scale)+shift, row-wise over the last dim (out bf16, or f32 in fp32 validation mode)."""
     _need(x, F32, "norm_modulate.x")
-    _need(out, BF16, "norm_modulate.out")
+    f32 = out.dtype == F32
+    _need(out, F32 if f32 else BF16, "norm_modulate.out")
     rows, hidden = x.shape
-    _run("norm_modulate", rows * hidden * (4 + 2) + (8 * rows * hidden if probe_prev is not None else 0), "aqb_norm_modulate", _p(x), x.stride(0), _p(shift), _p(scale), _p(out), out.stride(0), rows,
-                 hidden, float(eps), int(kind), _p(probe_prev), _p(probe_partials), _p(run_flag), int(run_if),
-                 _stream())
+    _run("norm_modulate", rows * hidden * (4 + out.element_size()) + (8 * rows * hidden if probe_prev is not None else 0),
+         "aqb_norm_modulate_f32" if f32 else "aqb_norm_modulate", _p(x), x.stride(0), _p(shift), _p(scale), _p(out),
+         out.stride(0), rows, hidden, float(eps), int(kind), _p(probe_prev), _p(probe_partials), _p(run_flag),
+         int(run_if), _stream())
     return out
 
 
 def gemm(a, w, out, bias=None, gate=None, epilogue="bf16", alpha=None, aux=None, run_flag=None, run_if=1):
-    """out = epilogue(a @ w.T + bias) on tcgen05 (a [M,K] bf16, w [N,K] bf16)."""
-    _need(a, BF16, "gemm.a")
+    """out = epilogue(a @ w.T + bias) on tcgen05 (a [M,K] bf16, w [N,K] bf16).
+
+    fp32 validation mode: ``a`` f32 selects the SIMT fp32 kernel (out/aux f32)."""
     _need(w, BF16, "gemm.w")
     m, k = a.shape
     n, k2 = w.shape
     if k2 != k:
         raise NativeError(f"gemm: K mismatch {k} vs {k2}")
     e = EPI[epilogue]
-    _need(out, BF16 if e in (0, 1) else F32, "gemm.out")
+    f32 = a.dtype == F32
+    _need(a, F32 if f32 else BF16, "gemm.a")
+    _need(out, F32 if (f32 or e not in (0, 1)) else BF16, "gemm.out")
     if out.shape[0] != m or out.shape[1] < n:
         raise NativeError(f"gemm: out shape {tuple(out.shape)} vs ({m},{n})")
-    _run("gemm", 2.0 * m * n * k, "aqb_gemm_bf16", _p(a), a.stride(0), _p(w), w.stride(0), _p(out), out.stride(0), m, n, k,
-                 _p(bias), _p(gate), e, _p(alpha), _p(aux), aux.stride(0) if aux is not None else 0,
-                 _p(run_flag), int(run_if), _stream())
+    _run("gemm", 2.0 * m * n * k, "aqb_gemm_f32" if f32 else "aqb_gemm_bf16", _p(a), a.stride(0), _p(w), w.stride(0),
+         _p(out), out.stride(0), m, n, k, _p(bias), _p(gate), e, _p(alpha), _p(aux),
+         aux.stride(0) if aux is not None else 0, _p(run_flag), int(run_if), _stream())
     return out
 
 
@@ -137,8 +142,11 @@ def gemm_qknorm_rope(a, w, out, part_width, norm_parts, q_w, k_w, eps, bias=None
 def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_row0=0, rope_rows=0,
                  dst=None, head_begin=0, head_count=None, hpg=None, dst_group_stride=0, dst_row_stride=None,
                  dst_which_stride=None, parts=3, norm_parts=2, run_flag=None, run_if=1):
-    """QK-RMSNorm + 3D RoPE over a [rows, parts, heads, D] buffer (optionally repacked into dst)."""
-    _need(src, BF16, "qk_norm_rope.src")
+    """QK-RMSNorm + 3D RoPE over a [rows, parts, heads, D] buffer (optionally repacked into dst).
+
+    bf16, or f32 (fp32 validation mode) — src and dst share the dtype."""
+    f32 = src.dtype == F32
+    _need(src, F32 if f32 else BF16, "qk_norm_rope.src")
     rows = src.shape[0]
     head_count = heads if head_count is None else head_count
     hpg = head_count if hpg is None else hpg
@@ -148,24 +156,79 @@ def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_r
         dst_row_stride = dst.stride(0)
     if dst_which_stride is None:
         dst_which_stride = heads * head_dim
-    _run("qk_norm_rope", 2 * rows * head_count * head_dim * parts * 2, "aqb_qk_norm_rope", _p(src), src.stride(0), rows, heads, head_begin, head_count, head_dim,
+    if dst.dtype != src.dtype:
+        raise NativeError("qk_norm_rope: src and dst dtypes differ")
+    _run("qk_norm_rope", 2 * rows * head_count * head_dim * parts * src.element_size(),
+         "aqb_qk_norm_rope_f32" if f32 else "aqb_qk_norm_rope", _p(src), src.stride(0), rows, heads, head_begin, head_count, head_dim,
                  _p(q_w), _p(k_w), float(eps), _p(cos), _p(sin), int(rope_row0), int(rope_rows), _p(dst),
                  int(dst_group_stride), int(dst_row_stride), int(dst_which_stride), int(hpg), int(parts),
                  int(norm_parts), _p(run_flag), int(run_if), _stream())
     return dst
 
 
+def attention_workspace_bytes(seq_q, seq_kv, heads, head_dim, splits=None):
+    """Workspace the split-KV path needs (0 when one pass is best)."""
+    if splits is None:
+        splits = _native.query("aqb_attention_splits", seq_q, seq_kv, heads, head_dim)
+    return int(_native.query("aqb_attention_workspace_bytes", seq_q, heads, head_dim, splits))
+
+
 def attention(q, k, v, o, heads, head_dim, q_head_stride=None, k_head_stride=None, v_head_stride=None,
-              o_head_stride=None, scale=None, run_flag=None, run_if=1):
-    """Non-causal flash attention; q/k/v/o are 2-D row views [seq, ld] (head h at column h*head_stride)."""
+              o_head_stride=None, scale=None, splits=0, workspace=None, run_flag=None, run_if=1):
+    """Non-causal flash attention; q/k/v/o are 2-D row views [seq, ld] (head h at column h*head_stride).
+
+    ``splits``: 0 = automatic split-KV (uses ``workspace`` when given, a uint8
+    CUDA tensor), 1 = single pass."""
+    f32 = q.dtype == F32
     for t, nm in ((q, "q"), (k, "k"), (v, "v"), (o, "o")):
-        _need(t, BF16, f"attention.{nm}")
+        _need(t, F32 if f32 else BF16, f"attention.{nm}")
     hs = lambda x: head_dim if x is None else x  # noqa: E731
     scale = head_dim ** -0.5 if scale is None else scale
-    _run("attention", 4.0 * q.shape[0] * k.shape[0] * head_dim * heads, "aqb_attention_fwd", _p(q), q.stride(0), hs(q_head_stride), _p(k), k.stride(0), hs(k_head_stride),
-                 _p(v), v.stride(0), hs(v_head_stride), _p(o), o.stride(0), hs(o_head_stride), q.shape[0],
-                 k.shape[0], heads, head_dim, float(scale), _p(run_flag), int(run_if), _stream())
+    if f32:  # fp32 validation mode
+        _run("attention", 4.0 * q.shape[0] * k.shape[0] * head_dim * heads, "aqb_attention_f32", _p(q), q.stride(0),
+             hs(q_head_stride), _p(k), k.stride(0), hs(k_head_stride), _p(v), v.stride(0), hs(v_head_stride), _p(o),
+             o.stride(0), hs(o_head_stride), q.shape[0], k.shape[0], heads, head_dim, float(scale), _p(run_flag),
+             int(run_if), _stream())
+        return o
+    ws, wsb = (_p(workspace), workspace.numel()) if workspace is not None else (None, 0)
+    _run("attention", 4.0 * q.shape[0] * k.shape[0] * head_dim * heads, "aqb_attention_fwd", _p(q), q.stride(0),
+         hs(q_head_stride), _p(k), k.stride(0), hs(k_head_stride), _p(v), v.stride(0), hs(v_head_stride), _p(o),
+         o.stride(0), hs(o_head_stride), q.shape[0], k.shape[0], heads, head_dim, float(scale), int(splits), ws, wsb,
+         _p(run_flag), int(run_if), _stream())
     return o
+
+
+def attention_scatter(q, k, v, peer_o, ldo, heads, head_dim, rows_per_rank, text_row0, scale=None, splits=0,
+                      workspace=None, run_flag=None, run_if=1):
+    """Attention whose epilogue stores each output row into the owning rank's O buffer (peer memory)."""
+    for t, nm in ((q, "q"), (k, "k"), (v, "v")):
+        _need(t, BF16, f"attention_scatter.{nm}")
+    scale = head_dim ** -0.5 if scale is None else scale
+    ws, wsb = (_p(workspace), workspace.numel()) if workspace is not None else (None, 0)
+    _run("attention", 4.0 * q.shape[0] * k.shape[0] * head_dim * heads, "aqb_attention_fwd_scatter", _p(q),
+         q.stride(0), head_dim, _p(k), k.stride(0), head_dim, _p(v), v.stride(0), head_dim,
+         _native.ptr_array(peer_o), len(peer_o), int(ldo), head_dim, int(rows_per_rank), int(text_row0), q.shape[0],
+         k.shape[0], heads, head_dim, float(scale), int(splits), ws, wsb, _p(run_flag), int(run_if), _stream())
+
+
+def gemm_qknorm_rope_scatter(a, w, peer_out, part_width, norm_parts, q_w, k_w, eps, out_row_stride, hpg, bias=None,
+                             cos=None, sin=None, rope_row0=0, rope_rows=0, run_flag=None, run_if=1):
+    """QKV projection + QK-RMSNorm + 3D RoPE whose epilogue stores head group g into rank g's buffer."""
+    _need(a, BF16, "gemm_qknorm_rope_scatter.a")
+    _need(w, BF16, "gemm_qknorm_rope_scatter.w")
+    m, k = a.shape
+    n = w.shape[0]
+    _run("gemm", 2.0 * m * n * k, "aqb_gemm_qknorm_rope_scatter", _p(a), a.stride(0), _p(w), w.stride(0), m, n, k,
+         _p(bias), int(part_width), int(norm_parts), _p(q_w), _p(k_w), float(eps), _p(cos), _p(sin), int(rope_row0),
+         int(rope_rows), _native.ptr_array(peer_out), len(peer_out), int(out_row_stride), int(hpg), _p(run_flag),
+         int(run_if), _stream())
+
+
+def peer_barrier(peer_signal, rank, epoch, status, payload=None, pay_out=None, run_flag=None, run_if=1):
+    """Stream-ordered barrier over peer memory (optionally summing a few floats in rank order)."""
+    npay = 0 if payload is None else payload.numel()
+    _run("peer", 0, "aqb_peer_barrier", _native.ptr_array(peer_signal), int(rank), len(peer_signal), _p(epoch),
+         _p(payload), npay, _p(pay_out), _p(status), _p(run_flag), int(run_if), _stream())
 
 
 def gemv(w, x, out, bias=None, add=None, in_silu=False, t=None):

@@ -9,9 +9,17 @@ replicated on every rank (their head slice is taken locally; their
 attention output is all-gathered).  The rel-L1 cache decision all-reduces two
 scalars so every rank takes the same branch.
 
-This module only wraps ``torch.distributed``; the packing into the
-all-to-all layout is fused into the QK-norm/RoPE kernel and the unpacking is
-the ``aqb_heads_to_seq`` kernel.
+Two exchange implementations:
+
+* ``p2p`` (default): no collective on the data path.  :class:`PeerBuffers`
+  allocates the attention-input and attention-output buffers in libaqb and
+  maps every rank's copy into every process (CUDA IPC over NVLink/NVSwitch);
+  the QKV-GEMM epilogue stores each head group straight into its owner's
+  input buffer, the attention epilogue stores each output row straight into
+  its owner's O buffer, and a device barrier kernel (``aqb_peer_barrier``)
+  orders them.  The rel-L1 sums ride on that barrier.
+* ``nccl``: ``all_to_all_single`` / ``all_gather`` between a packing epilogue
+  and ``aqb_heads_to_seq`` (kept as the measured baseline).
 """
 
 from __future__ import annotations
@@ -21,18 +29,32 @@ import os
 import torch
 import torch.distributed as dist
 
-from .errors import ConfigError
+from . import _native
+from .errors import ConfigError, NativeError
+
+
+EXCHANGES = ("p2p", "nccl")
+PEER_MAX_RANKS = 8          # one NVSwitch box
+IPC_HANDLE_BYTES = 64       # AQB_IPC_HANDLE_BYTES
+SIGNAL_BYTES = 512          # AQB_PEER_SIGNAL_BYTES
 
 
 class Ulysses:
     """Sequence-parallel group context (``P`` ranks, this rank ``rank``)."""
 
-    def __init__(self, group=None):
+    def __init__(self, group=None, exchange: str | None = None):
         if not dist.is_initialized():
             raise ConfigError("torch.distributed is not initialised", "parallel.group")
         self.group = group if group is not None else dist.group.WORLD
         self.P = dist.get_world_size(self.group)
         self.rank = dist.get_rank(self.group)
+        if exchange is None:
+            exchange = os.environ.get("AQB_ULYSSES", "p2p")
+        if exchange not in EXCHANGES:
+            raise ConfigError(f"exchange must be one of {EXCHANGES}", "parallel.exchange")
+        if exchange == "p2p" and self.P > PEER_MAX_RANKS:
+            raise ConfigError(f"p2p exchange supports up to {PEER_MAX_RANKS} ranks", "parallel.exchange")
+        self.exchange = exchange
 
     def check(self, num_heads: int, video_tokens: int):
         if num_heads % self.P:
@@ -61,3 +83,73 @@ def init_from_env(backend: str | None = None):
     if backend == "nccl":
         torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
     dist.init_process_group(backend=backend)
+
+
+class _DeviceBytes:
+    """``__cuda_array_interface__`` view of a libaqb allocation (so torch can wrap it)."""
+
+    def __init__(self, ptr: int, nbytes: int):
+        self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "data": (ptr, False), "version": 3,
+                                         "strides": None}
+
+
+class PeerBuffers:
+    """Named symmetric buffers: same sizes on every rank, every rank's copy mapped in every process.
+
+    ``local(name, shape, dtype)`` is this rank's buffer as a torch tensor;
+    ``ptrs(name, offset)`` the device addresses of all ranks' copies (+ a byte
+    offset), in rank order, for the scatter epilogues and the barrier.
+    Collective: every rank must construct it with the same ``sizes``.
+    """
+
+    def __init__(self, sp: Ulysses, sizes: dict, device):
+        import ctypes
+
+        self.sp, self.device = sp, torch.device(device)
+        self._own, self._opened, self._nbytes = {}, [], dict(sizes)
+        handles = {}
+        for name, nbytes in sizes.items():
+            nbytes = max(int(nbytes), 16)
+            ptr = ctypes.c_void_p()
+            h = ctypes.create_string_buffer(IPC_HANDLE_BYTES)
+            _native.call("aqb_peer_alloc", nbytes, ctypes.addressof(ptr), ctypes.addressof(h))
+            self._own[name] = int(ptr.value)
+            handles[name] = h.raw
+        gathered = [None] * sp.P
+        dist.all_gather_object(gathered, handles, group=sp.group)
+        self._all = {}
+        for name in sizes:
+            row = []
+            for r in range(sp.P):
+                if r == sp.rank:
+                    row.append(self._own[name])
+                    continue
+                ptr = ctypes.c_void_p()
+                hb = ctypes.create_string_buffer(gathered[r][name], IPC_HANDLE_BYTES)
+                _native.call("aqb_peer_open", ctypes.addressof(hb), ctypes.addressof(ptr))
+                row.append(int(ptr.value))
+                self._opened.append(int(ptr.value))
+            self._all[name] = row
+
+    def local(self, name: str, shape, dtype) -> torch.Tensor:
+        n = 1
+        for d in shape:
+            n *= int(d)
+        nbytes = n * torch.empty((), dtype=dtype).element_size()
+        if nbytes > self._nbytes[name]:
+            raise NativeError(f"peer buffer {name}: {nbytes} B requested, {self._nbytes[name]} allocated")
+        raw = torch.as_tensor(_DeviceBytes(self._own[name], nbytes), device=self.device)
+        return raw.view(dtype).view(*shape)
+
+    def ptrs(self, name: str, offset_bytes: int = 0) -> list:
+        return [p + int(offset_bytes) for p in self._all[name]]
+
+    def close(self):
+        """Unmap peers and free this rank's buffers (collective: barrier first)."""
+        dist.barrier(group=self.sp.group)
+        torch.cuda.synchronize()
+        for p in self._opened:
+            _native.call("aqb_peer_close", p)
+        for p in self._own.values():
+            _native.call("aqb_peer_free", p)
+        self._opened, self._own = [], {}

@@ -30,14 +30,25 @@ def rel(a, b):
 
 def main():
     init_from_env("nccl")
-    sp = Ulysses()
+    ok = True
+    for exchange in ("p2p", "nccl"):
+        ok &= run_cases(Ulysses(exchange=exchange))
+    flag = torch.tensor([1 if ok else 0], device="cuda")
+    dist.broadcast(flag, 0)
+    dist.destroy_process_group()
+    sys.exit(0 if int(flag) else 1)
+
+
+def run_cases(sp):
     P = sp.P
     ok = True
     cases = [
-        ("single", DiTConfig("single-dit", hidden_size=256, num_heads=8, num_single=4, text_dim=256, text_len=40),
+        ("single", DiTConfig("single-dit", hidden_size=1024, num_heads=8, num_single=4, text_dim=256, text_len=40),
          (3, 8, 16)),
-        ("mm", DiTConfig("mm-dit", hidden_size=256, num_heads=8, num_dual=2, num_single=2, text_dim=192, text_len=24,
+        ("mm", DiTConfig("mm-dit", hidden_size=1024, num_heads=8, num_dual=2, num_single=2, text_dim=192, text_len=24,
                          pooled_dim=64), (2, 8, 16)),
+        ("single-d32", DiTConfig("single-dit", hidden_size=256, num_heads=8, num_single=4, text_dim=256, text_len=40),
+         (3, 8, 16)),
     ]
     for name, cfg, grid in cases:
         W = init_weights(cfg, seed=0)
@@ -60,15 +71,14 @@ def main():
                 same = list(r_sp.schedule.per_step_full) == list(taken) == list(r1.schedule.per_step_full)
                 good = same and e_sp_o <= 1e-2 and e_sp_1 <= 5e-3
                 ok &= good
-                print(json.dumps({"case": name, "P": P, "cache": type(cache).__name__,
+                if m_sp.peer is not None and not m_sp.peer_ok():
+                    good = False
+                print(json.dumps({"case": name, "P": P, "exchange": sp.exchange, "cache": type(cache).__name__,
                                   "schedule": r_sp.schedule.as_string(), "same_schedule": same,
                                   "max_rel_l2_vs_1gpu": e_sp_1, "max_rel_l2_vs_oracle": e_sp_o, "ok": good}),
                       flush=True)
             dist.barrier()
-    flag = torch.tensor([1 if ok else 0], device="cuda")
-    dist.broadcast(flag, 0)
-    dist.destroy_process_group()
-    sys.exit(0 if int(flag) else 1)
+    return ok
 
 
 if __name__ == "__main__":

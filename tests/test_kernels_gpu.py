@@ -288,3 +288,108 @@ def test_gemm_qknorm_rope_ulysses_pack_and_local_heads():
     ops.gemm_qknorm_rope(a, w, loc, H, 2, qw, kw, 1e-6, bias=b, out_row_stride=3 * hl * 128, groups=1, hpg=hl, g_base=1)
     exp2 = _qkv_ref(a, w, b, qw, kw, heads, 0, cos, sin)
     assert rel_l2(loc, exp2[:, :, hl:]) < 6e-3
+
+
+def test_gemm_qknorm_rope_scatter_equals_pack():
+    """The peer-scatter epilogue (one TMA map per destination rank) writes exactly what the
+    packed all-to-all layout holds; destinations are local buffers standing in for peers."""
+    rows, heads, P = 700, 8, 4
+    hl, H = heads // P, heads * 128
+    rs = 3 * hl * 128
+    g = torch.Generator(device=dev).manual_seed(21)
+    a = torch.randn(rows, H, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(3 * H, H, device=dev, generator=g) * 0.03).to(torch.bfloat16)
+    b = torch.randn(3 * H, device=dev, generator=g) * 0.1
+    qw = 1 + 0.1 * torch.randn(128, device=dev, generator=g)
+    kw = 1 + 0.1 * torch.randn(128, device=dev, generator=g)
+    ang = torch.rand(P * rows, 64, device=dev, generator=g) * 6.28
+    cos, sin = torch.cos(ang), torch.sin(ang)
+    rank = 2
+    snd = torch.zeros(P, rows, 3, hl, 128, device=dev, dtype=torch.bfloat16)
+    ops.gemm_qknorm_rope(a, w, snd, H, 2, qw, kw, 1e-6, bias=b, cos=cos, sin=sin, rope_row0=rank * rows,
+                         rope_rows=P * rows, out_row_stride=rs, groups=P, group_stride=rows * rs, hpg=hl)
+    rcv = [torch.full((P * rows + 5, 3, hl, 128), 7.0, device=dev, dtype=torch.bfloat16) for _ in range(P)]
+    dst = [r.data_ptr() + rank * rows * rs * 2 for r in rcv]
+    ops.gemm_qknorm_rope_scatter(a, w, dst, H, 2, qw, kw, 1e-6, rs, hl, bias=b, cos=cos, sin=sin,
+                                 rope_row0=rank * rows, rope_rows=P * rows)
+    for r in range(P):
+        assert torch.equal(rcv[r][rank * rows:(rank + 1) * rows], snd[r])
+        assert bool((rcv[r][:rank * rows] == 7).all()) and bool((rcv[r][(rank + 1) * rows:] == 7).all())
+
+
+@pytest.mark.parametrize("sq,skv,heads,d,splits", [(7800 // 8 * 8 + 256, 8056, 2, 128, 0), (1000, 3000, 2, 128, 3),
+                                                   (300, 1000, 3, 128, 5), (200, 600, 4, 64, 2),
+                                                   (96, 400, 4, 32, 4), (257, 129, 1, 128, 2)])
+def test_attention_split_kv(sq, skv, heads, d, splits):
+    """Split-KV partials + combine equal the single-pass kernel (within bf16 rounding)."""
+    g = torch.Generator(device=dev).manual_seed(sq + skv + splits)
+    q = torch.randn(sq, heads * d, device=dev, generator=g).to(torch.bfloat16)
+    k = torch.randn(skv, heads * d, device=dev, generator=g).to(torch.bfloat16)
+    v = torch.randn(skv, heads * d, device=dev, generator=g).to(torch.bfloat16)
+    o1 = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
+    ops.attention(q, k, v, o1, heads, d, splits=1)
+    ns = splits or _native_splits(sq, skv, heads, d)
+    ws = torch.empty(ops.attention_workspace_bytes(sq, skv, heads, d, ns), device=dev, dtype=torch.uint8)
+    o2 = torch.empty_like(o1)
+    ops.attention(q, k, v, o2, heads, d, splits=splits, workspace=ws)
+    exp = _attn_ref(q.view(sq, heads, d), k.view(skv, heads, d), v.view(skv, heads, d))
+    assert rel_l2(o2, exp) < 1e-2
+    assert rel_l2(o2, o1) < 8e-3
+
+
+def _native_splits(sq, skv, heads, d):
+    from paper_2505_10584_b200 import _native
+    return _native.query("aqb_attention_splits", sq, skv, heads, d)
+
+
+def test_attention_auto_splits_for_few_heads():
+    """Ulysses at 8 GPUs leaves 2 heads per rank: the planner must split KV to fill the SMs."""
+    assert _native_splits(8056, 8056, 2, 128) >= 2
+    assert _native_splits(119056, 119056, 24, 128) == 1
+    assert _native_splits(7800, 256, 16, 128) == 1
+
+
+@pytest.mark.parametrize("splits", [1, 3])
+def test_attention_scatter_rows_to_owners(splits):
+    """Scatter epilogue: video row r -> rank r // rpr, text rows -> every rank (local stand-ins for peers)."""
+    P, rpr, St, hl, d = 4, 300, 40, 2, 128
+    H = P * hl * d
+    sq = P * rpr + St
+    g = torch.Generator(device=dev).manual_seed(5 + splits)
+    qkv = torch.randn(sq, 3, hl, d, device=dev, generator=g).to(torch.bfloat16)
+    flat = qkv.view(sq, -1)
+    ref_o = torch.empty(sq, hl * d, device=dev, dtype=torch.bfloat16)
+    ops.attention(flat, flat[:, hl * d:], flat[:, 2 * hl * d:], ref_o, hl, d, splits=splits,
+                  workspace=torch.empty(ops.attention_workspace_bytes(sq, sq, hl, d, splits), device=dev,
+                                        dtype=torch.uint8))
+    outs = [torch.zeros(rpr + St, H, device=dev, dtype=torch.bfloat16) for _ in range(P)]
+    rank = 1
+    dst = [o.data_ptr() + rank * hl * d * 2 for o in outs]
+    ws = torch.empty(ops.attention_workspace_bytes(sq, sq, hl, d, splits), device=dev, dtype=torch.uint8)
+    ops.attention_scatter(flat, flat[:, hl * d:], flat[:, 2 * hl * d:], dst, H, hl, d, rpr, P * rpr, splits=splits,
+                          workspace=ws)
+    cols = slice(rank * hl * d, (rank + 1) * hl * d)
+    for r in range(P):
+        assert torch.equal(outs[r][:rpr, cols], ref_o[r * rpr:(r + 1) * rpr])
+        assert torch.equal(outs[r][rpr:, cols], ref_o[P * rpr:])
+        assert float(outs[r][:, :rank * hl * d].abs().sum()) == 0.0  # other ranks' head columns untouched
+
+
+def test_peer_barrier_single_rank_payload():
+    """nranks=1: the barrier advances the epoch and returns the payload (sum over one rank)."""
+    import ctypes
+    from paper_2505_10584_b200 import _native
+
+    ptr, h = ctypes.c_void_p(), ctypes.create_string_buffer(64)
+    _native.call("aqb_peer_alloc", 512, ctypes.addressof(ptr), ctypes.addressof(h))
+    try:
+        epoch = torch.zeros(1, device=dev, dtype=torch.int32)
+        status = torch.zeros(1, device=dev, dtype=torch.int32)
+        pay = torch.tensor([1.5, -2.25], device=dev)
+        for i in range(3):
+            ops.peer_barrier([ptr.value], 0, epoch, status, payload=pay, pay_out=pay)
+        torch.cuda.synchronize()
+        assert int(epoch) == 3 and int(status) == 0
+        assert pay.tolist() == [1.5, -2.25]
+    finally:
+        _native.call("aqb_peer_free", ptr.value)

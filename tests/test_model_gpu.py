@@ -25,10 +25,11 @@ def rel_l2(a, b):
     return float((a - b).norm() / b.norm())
 
 
-def _setup(cfg, grid, steps_fraction=0.25):
+def _setup(cfg, grid, steps_fraction=0.25, precision="bf16"):
     W = init_weights(cfg, seed=0)
     inp = synthetic_inputs(cfg, grid)
-    model = build_model(cfg, weights=W).prepare(grid, inp["text"], inp["pooled"] if cfg.family == "mm-dit" else None)
+    model = build_model(cfg, weights=W, precision=precision).prepare(
+        grid, inp["text"], inp["pooled"] if cfg.family == "mm-dit" else None)
     orc = ref.OracleDiT(cfg, W, inp["text"], inp["pooled"] if cfg.family == "mm-dit" else None, grid,
                         n_front=front_block_count(cfg.num_layers, steps_fraction))
     return model, orc, inp
@@ -124,3 +125,45 @@ def test_full_2b_cache_interval1_equals_no_cache_and_is_deterministic():
     c = denoise(model, inp["x0"], 3, None).latent
     assert torch.isfinite(a).all()
     assert torch.equal(a, b) and torch.equal(a, c)
+
+
+TOL_FP32 = 1e-4
+
+
+@pytest.mark.parametrize("name", list(CASES))
+def test_fp32_validation_mode_matches_oracle(name):
+    """north_star fp32 validation mode: per-step latent rel-L2 <= 1e-4 and the same schedule."""
+    cfg, grid = CASES[name]
+    steps = 4 if name.startswith("tiny") else 6
+    sched = plan_cache(steps, warmup=1, interval=2)
+    model, orc, inp = _setup(cfg, grid, precision="fp32")
+    res = denoise(model, inp["x0"], steps, sched, trajectory=True)
+    lat, taken, _ = ref.denoise(orc, inp["x0"], steps, flags=sched.per_step_full)
+    assert res.schedule.per_step_full == tuple(taken)
+    _check_traj(res, lat, tol=TOL_FP32)
+
+
+def test_fp32_validation_mode_rel_l1_policy():
+    cfg, grid = CASES["single-d128"]
+    model, orc, inp = _setup(cfg, grid, precision="fp32")
+    _, _, probe = ref.denoise(orc, inp["x0"], 4, policy=RelL1Policy(threshold=1e9, warmup=1))
+    thr = 2.5 * sorted(probe[1:])[len(probe[1:]) // 2]
+    pol = RelL1Policy(threshold=thr, warmup=2)
+    lat, taken, rels = ref.denoise(orc, inp["x0"], 10, policy=pol)
+    res = denoise(model, inp["x0"], 10, pol, trajectory=True)
+    assert list(res.schedule.per_step_full) == taken
+    for g, r in zip(res.rel_l1[1:], rels[1:]):
+        assert abs(g - r) <= 1e-4 * abs(r) + 1e-7  # fp32 probe tracks the oracle tightly
+    _check_traj(res, lat, tol=TOL_FP32)
+
+
+def test_mmdit_13b_dims_two_blocks_match_oracle():
+    """MM-DiT 13.4B dims (H=3072, 24 heads, text 256x4096): 1 dual + 1 single block at a reduced
+    720p-like geometry (8x30x53 = 12,720 video + 256 text tokens), 2 steps, bf16 gate 1e-2."""
+    from paper_2505_10584_b200.config import MM_DIT_13B
+    cfg = with_overrides(MM_DIT_13B, num_dual=1, num_single=1)
+    grid = (8, 30, 53)
+    model, orc, inp = _setup(cfg, grid)
+    res = denoise(model, inp["x0"], 2, None, trajectory=True)
+    lat, _, _ = ref.denoise(orc, inp["x0"], 2, flags=[True, True])
+    _check_traj(res, lat)

@@ -29,7 +29,7 @@ def test_header_symbols_exported(lib_path):
 
 def test_abi_version_and_error_string(lib_path):
     lib = _native.load()
-    assert lib.aqb_abi_version() == 1
+    assert lib.aqb_abi_version() == 2
     assert isinstance(lib.aqb_last_error(), bytes)
 
 
@@ -39,7 +39,7 @@ def test_invalid_args_fail_loudly_without_gpu(lib_path):
     rc = lib.aqb_gemm_bf16(None, 0, None, 0, None, 0, 0, 0, 0, None, None, 0, None, None, 0, None, 1, None)
     assert rc == -1
     assert b"null pointer" in lib.aqb_last_error()
-    rc = lib.aqb_attention_fwd(1, 8, 8, 1, 8, 8, 1, 8, 8, 1, 8, 8, 16, 16, 1, 48, 1.0, None, 1, None)
+    rc = lib.aqb_attention_fwd(1, 8, 8, 1, 8, 8, 1, 8, 8, 1, 8, 8, 16, 16, 1, 48, 1.0, 0, None, 0, None, 1, None)
     assert rc == -1 and b"head_dim" in lib.aqb_last_error()
 
 
@@ -60,3 +60,21 @@ def test_sass_is_blackwell_native(lib_path):
     for mnem in ("UTCHMMA", "LDTM", "UTMALDG"):
         assert mnem in out, mnem
     assert "HMMA" not in out.replace("UTCHMMA", "")
+
+
+def test_attention_split_planner_and_workspace_without_gpu(lib_path):
+    """Host-side split-KV planner (SM count falls back to 148 without a GPU) and workspace sizing."""
+    lib = _native.load()
+    assert lib.aqb_attention_splits(8056, 8056, 2, 128) >= 2       # 2 heads x 32 tiles << 148 SMs
+    assert lib.aqb_attention_splits(119056, 119056, 24, 128) == 1  # 10k CTAs: no split
+    assert lib.aqb_attention_workspace_bytes(1000, 4, 128, 1) == 0
+    rows = 3 * 4 * 1000
+    assert lib.aqb_attention_workspace_bytes(1000, 4, 128, 3) == ((rows + 63) // 64 * 64 + rows * 128) * 4
+
+
+def test_peer_barrier_validates_before_launch(lib_path):
+    lib = _native.load()
+    assert lib.aqb_peer_barrier(None, 0, 2, None, None, 0, None, None, None, 1, None) == -1
+    arr = _native.ptr_array([16, 32])
+    assert lib.aqb_peer_barrier(arr, 2, 2, 64, None, 0, None, None, None, 1, None) == -1  # rank out of range
+    assert lib.aqb_peer_barrier(arr, 0, 9, 64, None, 0, None, None, None, 1, None) == -1  # > 8 ranks
