@@ -207,6 +207,27 @@ int aqb_heads_to_seq(const void* src, int64_t rows, int32_t P, int32_t width, vo
                      const int32_t* run_flag, int32_t run_if, void* stream);
 
 /* ---------------------------------------------------------------------------
+ * Either side of the denoise loop.
+ * aqb_tile_blend — VAE tile blend (plan: inference.py:89-226):
+ *   out[c, p] = sum_k prof_k(p) * tile_k[c, p - start_k] / sum_k prof_k(p), p = (t, h, w)
+ *   over the tiles covering p, where prof_k is the product of per-axis ramps
+ *   (rise (j+1)/(e+1) over the first e = min(overlap, size) entries, fall over the
+ *   last e).  Tiles form the plan's grid: axis_starts = [t-starts (nt) | h-starts (nh)
+ *   | w-starts (nw)] (device int32, ascending), tile_ptrs[(it*nh+ih)*nw+iw] = device
+ *   address (int64, device array) of tile f32 [C, tile_t, tile_h, tile_w] (may be peer
+ *   memory).  out f32 [C, T, H, W].  fp64 accumulation in plan order.
+ * aqb_window_average — temporal MultiDiffusion Eq. 3 (inference.py:229-279):
+ *   out[c, i, :] = (sum_{k: s_k <= i < s_k + n} clip_k[c, i - s_k, :]) / |S(i)|,
+ *   clip_ptrs (device int64) -> f32 [C, n, hw]; clip_starts device int32; out f32
+ *   [C, n_prime, hw]; sum in clip order.
+ */
+int aqb_tile_blend(const int64_t* tile_ptrs, const int32_t* axis_starts, int32_t nt, int32_t nh, int32_t nw,
+                   int32_t tile_t, int32_t tile_h, int32_t tile_w, int32_t ov_t, int32_t ov_h, int32_t ov_w, int32_t T,
+                   int32_t H, int32_t W, int32_t C, float* out, void* stream);
+int aqb_window_average(const int64_t* clip_ptrs, const int32_t* clip_starts, int32_t nclips, int32_t n,
+                       int32_t n_prime, int32_t C, int64_t hw, float* out, void* stream);
+
+/* ---------------------------------------------------------------------------
  * fp32 validation mode (north_star: <= 1e-4 latent rel-L2 vs the CPU
  * reference).  Same semantics as the bf16 entries above with every activation
  * in f32: aqb_norm_modulate_f32 writes f32 y; aqb_qk_norm_rope_f32 reads and

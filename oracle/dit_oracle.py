@@ -14,6 +14,7 @@ Paper anchors
 * QK-norm / LayerNorm+scale/shift / gate / GeLU ops: PAPER.md:253-256
 * Flow matching X_t=(1-t)X0+tX1, v = X1-X0: PAPER.md:127-131 (Euler sampler: fitted)
 * DiT-layer-output cache (rear-block offset reuse; no caching in warmup): PAPER.md:309,316
+* Attention cache (per-block attention output reuse): PAPER.md:313
 * Static schedule flags: ditplan ``inference.py:71-76`` (see schedule_oracle.py)
 """
 
@@ -138,11 +139,22 @@ def _qkv(W, p, m, cfg, ang):
     return q, k, v
 
 
+def _cached(cache, key, fn):
+    """Attention-cache mode: on a full step compute and store the
+    attention output of this block; on a cached step reuse the stored one."""
+    if cache is None:
+        return fn()
+    store, full = cache
+    if full or key not in store:
+        store[key] = fn()
+    return store[key]
+
+
 def _mlp(W, p, m):
     return linear(W, f"{p}.fc2", gelu(linear(W, f"{p}.fc1", m)))
 
 
-def single_dit_block(W, i, x, tmod, text, cfg, ang):
+def single_dit_block(W, i, x, tmod, text, cfg, ang, cache=None):
     """One Single-DiT block (PixArt-α AdaLN-single layout).
 
     mods = t_block(SiLU(t)) + table_i  →  shift1, scale1, gate1, shift2, scale2, gate2
@@ -156,17 +168,21 @@ def single_dit_block(W, i, x, tmod, text, cfg, ang):
     mods = (tmod + _w(W, f"{p}.table")).reshape(6, H)
     sh1, sc1, g1, sh2, sc2, g2 = mods
     m = modulate(x, sh1, sc1, cfg.norm_eps)
-    q, k, v = _qkv(W, p, m, cfg, ang)
-    x = x + g1 * linear(W, f"{p}.proj", attention(q, k, v))
-    xq = rms_norm(linear(W, f"{p}.xq", x).reshape(-1, A, D), _w(W, f"{p}.xq_norm"), cfg.qk_norm_eps)
-    kv = linear(W, f"{p}.xkv", text).reshape(-1, 2, A, D)
-    xk = rms_norm(kv[:, 0], _w(W, f"{p}.xk_norm"), cfg.qk_norm_eps)
-    x = x + linear(W, f"{p}.xproj", attention(xq, xk, kv[:, 1]))
+    o = _cached(cache, ("self", i), lambda: attention(*_qkv(W, p, m, cfg, ang)))
+    x = x + g1 * linear(W, f"{p}.proj", o)
+
+    def cross():
+        xq = rms_norm(linear(W, f"{p}.xq", x).reshape(-1, A, D), _w(W, f"{p}.xq_norm"), cfg.qk_norm_eps)
+        kv = linear(W, f"{p}.xkv", text).reshape(-1, 2, A, D)
+        xk = rms_norm(kv[:, 0], _w(W, f"{p}.xk_norm"), cfg.qk_norm_eps)
+        return attention(xq, xk, kv[:, 1])
+
+    x = x + linear(W, f"{p}.xproj", _cached(cache, ("cross", i), cross))
     x = x + g2 * _mlp(W, p, modulate(x, sh2, sc2, cfg.norm_eps))
     return x, m
 
 
-def mm_dual_block(W, i, img, txt, vec, cfg, ang):
+def mm_dual_block(W, i, img, txt, vec, cfg, ang, cache=None):
     """MM-DiT dual-stream block: separate weights per stream,
     joint attention over concat(video, text); RoPE on video tokens only."""
     H = cfg.hidden_size
@@ -175,9 +191,13 @@ def mm_dual_block(W, i, img, txt, vec, cfg, ang):
     mt = linear(W, f"dual.{i}.txt.mod", sv).reshape(6, H)
     m_img = modulate(img, mi[0], mi[1], cfg.norm_eps)
     m_txt = modulate(txt, mt[0], mt[1], cfg.norm_eps)
-    qi, ki, vi = _qkv(W, f"dual.{i}.img", m_img, cfg, ang)
-    qt, kt, vt = _qkv(W, f"dual.{i}.txt", m_txt, cfg, None)
-    o = attention(torch.cat([qi, qt]), torch.cat([ki, kt]), torch.cat([vi, vt]))
+
+    def joint():
+        qi, ki, vi = _qkv(W, f"dual.{i}.img", m_img, cfg, ang)
+        qt, kt, vt = _qkv(W, f"dual.{i}.txt", m_txt, cfg, None)
+        return attention(torch.cat([qi, qt]), torch.cat([ki, kt]), torch.cat([vi, vt]))
+
+    o = _cached(cache, ("dual", i), joint)
     n = img.shape[0]
     img = img + mi[2] * linear(W, f"dual.{i}.img.proj", o[:n])
     txt = txt + mt[2] * linear(W, f"dual.{i}.txt.proj", o[n:])
@@ -186,13 +206,13 @@ def mm_dual_block(W, i, img, txt, vec, cfg, ang):
     return img, txt, m_img
 
 
-def mm_single_block(W, i, x, vec, cfg, ang):
+def mm_single_block(W, i, x, vec, cfg, ang, cache=None):
     """MM-DiT single-stream joint block over [video; text] with shared weights."""
     H = cfg.hidden_size
     md = linear(W, f"single.{i}.mod", silu(vec)).reshape(6, H)
     m = modulate(x, md[0], md[1], cfg.norm_eps)
-    q, k, v = _qkv(W, f"single.{i}", m, cfg, ang)
-    x = x + md[2] * linear(W, f"single.{i}.proj", attention(q, k, v))
+    o = _cached(cache, ("single", i), lambda: attention(*_qkv(W, f"single.{i}", m, cfg, ang)))
+    x = x + md[2] * linear(W, f"single.{i}.proj", o)
     x = x + md[5] * _mlp(W, f"single.{i}", modulate(x, md[3], md[4], cfg.norm_eps))
     return x, m
 
@@ -208,10 +228,14 @@ class OracleDiT:
     then either the rear blocks (``full``; the offset
     ``rear_out - rear_in`` of the video tokens is stored in ``state``) or adds
     the stored offset (cached step) — PAPER.md:309.  Returns ``(v, m0)``.
+    ``mode="attention-cache"`` runs every block and reuses each
+    block's attention output (pre-projection) from the last full step instead.
     """
 
-    def __init__(self, cfg, weights: dict, text: torch.Tensor, pooled: torch.Tensor | None, grid, n_front=None):
+    def __init__(self, cfg, weights: dict, text: torch.Tensor, pooled: torch.Tensor | None, grid, n_front=None,
+                 mode: str = "dit-layer-cache"):
         self.cfg = cfg
+        self.mode = mode
         self.W = {k: v.detach().to("cpu", f32) for k, v in weights.items()}
         self.text = text.to("cpu", f32)
         self.pooled = None if pooled is None else pooled.to("cpu", f32)
@@ -229,6 +253,10 @@ class OracleDiT:
         n = x_tok.shape[0]
         nl = cfg.num_layers if blocks is None else blocks
         nf = min(self.n_front, nl)
+        cache = None
+        if self.mode == "attention-cache":
+            cache = (state.setdefault("attn", {}) if state is not None else {}, full)
+            nf, full = nl, True  # every block runs; no rear-block offset
         t0 = self._temb(t)
         m0 = None
         if cfg.family == "single-dit":
@@ -240,7 +268,7 @@ class OracleDiT:
                         x = x + state["offset"]
                         break
                     x_in = x
-                x, m = single_dit_block(W, i, x, tmod, self.text, cfg, self.ang)
+                x, m = single_dit_block(W, i, x, tmod, self.text, cfg, self.ang, cache)
                 if i == 0:
                     m0 = m
             if full and nf < nl:
@@ -262,11 +290,11 @@ class OracleDiT:
                     break
                 img_in = cur
             if i < cfg.num_dual:
-                img, txt, m = mm_dual_block(W, i, img, txt, vec, cfg, self.ang)
+                img, txt, m = mm_dual_block(W, i, img, txt, vec, cfg, self.ang, cache)
             else:
                 if x is None:
                     x = torch.cat([img, txt])
-                x, m = mm_single_block(W, i - cfg.num_dual, x, vec, cfg, self.ang)
+                x, m = mm_single_block(W, i - cfg.num_dual, x, vec, cfg, self.ang, cache)
                 img = x[:n]
             if i == 0:
                 m0 = m[:n]

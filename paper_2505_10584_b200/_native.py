@@ -49,6 +49,9 @@ SIGNATURES = {
                              c_int64, P, c_int32, P]),
     "aqb_attention_f32": (c_int, [P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64,
                                   c_int64, c_int64, c_int64, c_int32, c_int32, c_float, P, c_int32, P]),
+    "aqb_tile_blend": (c_int, [P, P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
+                               c_int32, c_int32, c_int32, c_int32, P, P]),
+    "aqb_window_average": (c_int, [P, P, c_int32, c_int32, c_int32, c_int32, c_int64, P, P]),
     "aqb_peer_alloc": (c_int, [c_int64, P, P]),
     "aqb_peer_open": (c_int, [P, P]),
     "aqb_peer_close": (c_int, [P]),

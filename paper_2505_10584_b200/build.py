@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(os.path.dirname(HERE), "include")
 LIB = os.path.join(HERE, "libaqb.so")
-SOURCES = ["host.cu", "elementwise.cu", "gemm.cu", "attention.cu", "peer.cu", "fp32.cu"]
+SOURCES = ["host.cu", "elementwise.cu", "gemm.cu", "attention.cu", "peer.cu", "fp32.cu", "tiles.cu"]
 HEADERS = ["ptx.cuh", "host.cuh"]
 
 NVCC_FLAGS = [

@@ -23,6 +23,7 @@
 // TMEM: S0 | S1 | O0 | O1  (128 + 128 + D + D columns).
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 
 #include "host.cuh"
 #include "ptx.cuh"
@@ -67,6 +68,16 @@ struct OutMap {
   int64_t rows_per_rank, text_row0;
 };
 
+// TMA store maps of the output (3-D: d, head, row; box 64 x 1 x 128).  Local:
+// `local` over o[seq_q].  Scatter: vid[r] over rank r's rows_per_rank video
+// rows, txt[r] over its text rows (so a tile straddling a rank boundary is
+// clipped by each map, never spilling into the neighbour's rows).
+struct OutMaps {
+  CUtensorMap local;
+  CUtensorMap vid[kMaxPeers];
+  CUtensorMap txt[kMaxPeers];
+};
+
 struct Params {
   int seq_q, seq_kv, heads, head_dim;
   float scale_log2;
@@ -98,7 +109,7 @@ __device__ __forceinline__ void for_each_out(const OutMap& m, int head, int64_t 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-                    const __grid_constant__ CUtensorMap tv, Params p) {
+                    const __grid_constant__ CUtensorMap tv, const __grid_constant__ OutMaps om, Params p) {
   using C = Cfg<D>;
   if (!gate_open(p.run_flag, p.run_if)) return;
   extern __shared__ uint8_t smem_raw[];
@@ -347,24 +358,48 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
     } else {
+      // O/l -> bf16 into this tile's Q buffer (idle once its last QK^T is done; same
+      // 128B-swizzled [64-col box][128 rows][128 B] layout), then TMA stores: coalesced,
+      // and under the Ulysses scatter straight into the owning ranks' buffers.
+      uint8_t* stile = sQ + t * C::kQBytes;
+      const uint32_t srow = smem_u32(stile) + r * 128;
 #pragma unroll 1
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t u[32];
         tmem_ld32(o_tmem + cc * 32, u);
         tmem_wait_ld();
-        if (live && cc * 32 < p.head_dim) {
-          uint4 pk[4];
+        const uint32_t bx = srow + (cc >> 1) * (BQ * 128);
 #pragma unroll
-          for (int g = 0; g < 4; ++g)
-            pk[g] = make_uint4(pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
-                               pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
-                               pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
-                               pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
-          for_each_out(p.out, head, row, [&](__nv_bfloat16* orow) {
-#pragma unroll
-            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = pk[g];
-          });
+        for (int g = 0; g < 4; ++g)
+          st_shared_v4(bx + ((((cc & 1) * 4 + g) ^ sw) << 4),
+                       pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
+                       pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
+                       pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
+                       pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1 + t, 128);
+      if (quad == 0 && lane == 0) {
+        const int tr0 = q0 + t * BQ;  // first row of this tile
+        const OutMap& m = p.out;
+        for (int c = 0; c < C::kBoxes; ++c) {
+          const uint8_t* src = stile + c * (BQ * 128);
+          if (m.nranks == 0) {
+            tma_store_3d(&om.local, src, c * 64, head, tr0);
+          } else {
+            const int64_t vend = (tr0 + BQ < m.text_row0) ? int64_t(tr0 + BQ) : m.text_row0;
+            if (tr0 < vend) {
+              const int r0 = int(tr0 / m.rows_per_rank), r1 = int((vend - 1) / m.rows_per_rank);
+              for (int rr = r0; rr <= r1; ++rr)
+                tma_store_3d(&om.vid[rr], src, c * 64, head, int(tr0 - rr * m.rows_per_rank));
+            }
+            if (tr0 + BQ > m.text_row0)
+              for (int rr = 0; rr < m.nranks; ++rr)
+                tma_store_3d(&om.txt[rr], src, c * 64, head, int(tr0 - m.text_row0));
+          }
         }
+        bulk_commit();
+        bulk_wait<0>();  // complete (not just read out of smem) before the CTA exits
       }
     }
   } else {
@@ -427,6 +462,31 @@ int choose_splits(int64_t seq_q, int64_t seq_kv, int heads, int head_dim) {
   return bs;
 }
 
+// Output TMA maps for p.out (see OutMaps).
+static int make_out_maps(const Params& p, OutMaps& om) {
+  memset(&om, 0, sizeof(om));
+  const OutMap& m = p.out;
+  const uint64_t str[2] = {uint64_t(m.o_head_stride) * 2, uint64_t(m.ldo) * 2};
+  const uint32_t box[3] = {64, 1, 128};
+  if (m.nranks == 0) {
+    const uint64_t dims[3] = {uint64_t(p.head_dim), uint64_t(p.heads), uint64_t(p.seq_q)};
+    return make_tmap_bf16(&om.local, m.o, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+  }
+  const int64_t text_rows = p.seq_q - m.text_row0;
+  for (int r = 0; r < m.nranks; ++r) {
+    const uint64_t dv[3] = {uint64_t(p.head_dim), uint64_t(p.heads), uint64_t(m.rows_per_rank)};
+    int rc = make_tmap_bf16(&om.vid[r], m.peer_o[r], 3, dv, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    if (text_rows > 0) {
+      const uint64_t dt[3] = {uint64_t(p.head_dim), uint64_t(p.heads), uint64_t(text_rows)};
+      rc = make_tmap_bf16(&om.txt[r], m.peer_o[r] + m.rows_per_rank * m.ldo, 3, dt, str, box,
+                          CU_TENSOR_MAP_SWIZZLE_128B);
+      if (rc) return rc;
+    }
+  }
+  return AQB_OK;
+}
+
 template <int D>
 int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, int64_t khs, const void* v,
            int64_t ldv, int64_t vhs, const Params& p, cudaStream_t stream) {
@@ -456,8 +516,15 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     AQB_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
+  OutMaps om;
+  if (p.splits == 1) {
+    int rc = make_out_maps(p, om);
+    if (rc) return rc;
+  } else {
+    memset(&om, 0, sizeof(om));
+  }
   dim3 grid((p.seq_q + 2 * BQ - 1) / (2 * BQ), p.heads, p.splits);
-  attn_fwd_kernel<D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, p);
+  attn_fwd_kernel<D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, om, p);
   AQB_LAUNCH_CHECK();
   if (p.splits > 1) {
     const int64_t warps = static_cast<int64_t>(p.seq_q) * p.heads;

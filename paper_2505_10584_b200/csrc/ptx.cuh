@@ -277,6 +277,12 @@ AQB_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int32_t x, int3
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+AQB_DEV void tma_store_3d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1, int32_t c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
 AQB_DEV void tma_store_5d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1, int32_t c2, int32_t c3,
                           int32_t c4) {
   asm volatile("cp.async.bulk.tensor.5d.global.shared::cta.bulk_group [%0, {%2, %3, %4, %5, %6}], [%1];" ::"l"(

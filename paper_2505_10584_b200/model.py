@@ -182,6 +182,8 @@ class DiTModel:
             self.txt0 = e(St, H, dt=F32)
             ops.gemm(t_bf, W["txt_in.w"], self.txt0, bias=W["txt_in.b"], epilogue="f32")
         self.peer = None
+        self.ocache = self.xocache = None
+        self.cache_mode = "dit-layer-cache"
         hl = A // P
         self.hl = hl
         if self.sp is not None and P > 1:
@@ -233,7 +235,8 @@ class DiTModel:
         return [self.allmods[o + k * H:o + (k + 1) * H] for k in range(n)]
 
     def _qkv_attention(self, pi, pt, flag, run_if):
-        """QKV projection(s) + QK-RMSNorm + 3D RoPE + joint self-attention -> self.o.
+        """QKV projection(s) + QK-RMSNorm + 3D RoPE + joint self-attention -> self._ob
+        (``self.o``, or this block's attention-cache slot).
 
         ``pi``: weight prefix of the video stream (rows [0, Sv_loc)); ``pt``:
         prefix of the text rows [Sv_loc, rows) (MM-DiT; == pi for single
@@ -273,7 +276,7 @@ class DiTModel:
                 if St:
                     ops.qk_norm_rope(qkv[n:], A, D, W[f"{pt}.q_norm"], W[f"{pt}.k_norm"], eps, run_flag=flag,
                                      run_if=run_if)
-            ops.attention(qkv, qkv[:, H:], qkv[:, 2 * H:], self.o, A, D, workspace=self.attn_ws, run_flag=flag,
+            ops.attention(qkv, qkv[:, H:], qkv[:, 2 * H:], self._ob, A, D, workspace=self.attn_ws, run_flag=flag,
                           run_if=run_if)
             return
         sp, P, hl = self.sp, self.sp.P, self.hl
@@ -290,7 +293,7 @@ class DiTModel:
                                      run_flag=flag, run_if=run_if)
             self._barrier(flag, run_if)
             q = rcv.view(g.Sv + St, -1)
-            ops.attention_scatter(q, q[:, hl * D:], q[:, 2 * hl * D:], self.o_dst, H, hl, D, n, g.Sv,
+            ops.attention_scatter(q, q[:, hl * D:], q[:, 2 * hl * D:], self._odst, H, hl, D, n, g.Sv,
                                   workspace=self.attn_ws, run_flag=flag, run_if=run_if)
             self._barrier(flag, run_if)
             return
@@ -320,10 +323,10 @@ class DiTModel:
         ops.attention(q, q[:, hl * D:], q[:, 2 * hl * D:], self.oh, hl, D, workspace=self.attn_ws, run_flag=flag,
                       run_if=run_if)
         sp.all_to_all(self.ob.view(-1), self.oh[:g.Sv].reshape(-1))
-        ops.heads_to_seq(self.ob, n, P, hl * D, self.o[:n], run_flag=flag, run_if=run_if)
+        ops.heads_to_seq(self.ob, n, P, hl * D, self._ob[:n], run_flag=flag, run_if=run_if)
         if St:
             sp.all_gather(self.tg.view(-1), self.oh[g.Sv:].reshape(-1))
-            ops.heads_to_seq(self.tg, St, P, hl * D, self.o[n:], run_flag=flag, run_if=run_if)
+            ops.heads_to_seq(self.tg, St, P, hl * D, self._ob[n:], run_flag=flag, run_if=run_if)
 
     def _mlp(self, p, r0, r1, mods, flag, run_if):
         """x += gate2 * fc2(gelu(fc1(norm_mod(x, shift2, scale2))))  on rows [r0, r1)."""
@@ -335,79 +338,133 @@ class DiTModel:
                  run_if=run_if)
 
     # ----------------------------------------------------------------- blocks
-    def _single_dit_block(self, i, flag, run_if, probe):
+    def _single_dit_block(self, i, flag, run_if, probe, ag):
         cfg, g, W = self.cfg, self.geo, self.W
         A, D, H, eps = cfg.num_heads, cfg.head_dim, cfg.hidden_size, cfg.norm_eps
         p = f"blocks.{i}"
         mods = self._mod(i)
         n = g.Sv_loc
+        askip, aflag, arun = ag
         ops.norm_modulate(self.x, mods[0], mods[1], self.m, eps, probe_prev=self.prev if probe else None,
                           probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
         if probe:
             self._decide()
-        self._qkv_attention(p, None, flag, run_if)
-        ops.gemm(self.o, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=mods[2], epilogue="gate_res",
+        if not askip:
+            self._qkv_attention(p, None, aflag, arun)
+        ops.gemm(self._ob, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=mods[2], epilogue="gate_res",
                  run_flag=flag, run_if=run_if)
         # cross-attention to the text (no norm before it, PixArt-α); K/V precomputed per call
-        ops.norm_modulate(self.x, None, None, self.m, eps, kind=2, run_flag=flag, run_if=run_if)
-        ops.gemm(self.m, W[f"{p}.xq.w"], self.xq, bias=W[f"{p}.xq.b"], run_flag=flag, run_if=run_if)
-        ops.qk_norm_rope(self.xq, A, D, W[f"{p}.xq_norm"], None, cfg.qk_norm_eps, parts=1, norm_parts=1,
-                         run_flag=flag, run_if=run_if)
-        kv = self.text_kv[i]
-        ops.attention(self.xq, kv, kv[:, H:], self.o, A, D, workspace=self.attn_ws, run_flag=flag, run_if=run_if)
-        ops.gemm(self.o, W[f"{p}.xproj.w"], self.x, bias=W[f"{p}.xproj.b"], epilogue="gate_res", run_flag=flag,
+        xo = self._xo
+        if not askip:
+            ops.norm_modulate(self.x, None, None, self.m, eps, kind=2, run_flag=aflag, run_if=arun)
+            ops.gemm(self.m, W[f"{p}.xq.w"], self.xq, bias=W[f"{p}.xq.b"], run_flag=aflag, run_if=arun)
+            ops.qk_norm_rope(self.xq, A, D, W[f"{p}.xq_norm"], None, cfg.qk_norm_eps, parts=1, norm_parts=1,
+                             run_flag=aflag, run_if=arun)
+            kv = self.text_kv[i]
+            ops.attention(self.xq, kv, kv[:, H:], xo, A, D, workspace=self.attn_ws, run_flag=aflag, run_if=arun)
+        ops.gemm(xo, W[f"{p}.xproj.w"], self.x, bias=W[f"{p}.xproj.b"], epilogue="gate_res", run_flag=flag,
                  run_if=run_if)
         self._mlp(p, 0, n, mods, flag, run_if)
 
-    def _mm_dual_block(self, i, flag, run_if, probe):
+    def _mm_dual_block(self, i, flag, run_if, probe, ag):
         cfg, g, W, eps = self.cfg, self.geo, self.W, self.cfg.norm_eps
         n, R = g.Sv_loc, g.rows
         pi, pt = f"dual.{i}.img", f"dual.{i}.txt"
         mi, mt = self._mod(f"{pi}.mod"), self._mod(f"{pt}.mod")
-        ops.norm_modulate(self.x[:n], mi[0], mi[1], self.m[:n], eps, probe_prev=self.prev if probe else None,
-                          probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
+        askip, aflag, arun = ag
+        if probe or not askip:
+            ops.norm_modulate(self.x[:n], mi[0], mi[1], self.m[:n], eps, probe_prev=self.prev if probe else None,
+                              probe_partials=self.partials if probe else None,
+                              run_flag=flag if probe else aflag, run_if=run_if if probe else arun)
         if probe:
             self._decide()
-        ops.norm_modulate(self.x[n:], mt[0], mt[1], self.m[n:], eps, run_flag=flag, run_if=run_if)
-        self._qkv_attention(pi, pt, flag, run_if)
-        ops.gemm(self.o[:n], W[f"{pi}.proj.w"], self.x[:n], bias=W[f"{pi}.proj.b"], gate=mi[2], epilogue="gate_res",
+        if not askip:
+            ops.norm_modulate(self.x[n:], mt[0], mt[1], self.m[n:], eps, run_flag=aflag, run_if=arun)
+            self._qkv_attention(pi, pt, aflag, arun)
+        o = self._ob
+        ops.gemm(o[:n], W[f"{pi}.proj.w"], self.x[:n], bias=W[f"{pi}.proj.b"], gate=mi[2], epilogue="gate_res",
                  run_flag=flag, run_if=run_if)
-        ops.gemm(self.o[n:], W[f"{pt}.proj.w"], self.x[n:], bias=W[f"{pt}.proj.b"], gate=mt[2], epilogue="gate_res",
+        ops.gemm(o[n:], W[f"{pt}.proj.w"], self.x[n:], bias=W[f"{pt}.proj.b"], gate=mt[2], epilogue="gate_res",
                  run_flag=flag, run_if=run_if)
         self._mlp(pi, 0, n, mi, flag, run_if)
         self._mlp(pt, n, R, mt, flag, run_if)
 
-    def _mm_single_block(self, i, flag, run_if, probe):
+    def _mm_single_block(self, i, flag, run_if, probe, ag):
         cfg, g, W, eps = self.cfg, self.geo, self.W, self.cfg.norm_eps
         n, R = g.Sv_loc, g.rows
         p = f"single.{i}"
         md = self._mod(f"{p}.mod")
+        askip, aflag, arun = ag
         if probe:
             ops.norm_modulate(self.x[:n], md[0], md[1], self.m[:n], eps, probe_prev=self.prev,
                               probe_partials=self.partials, run_flag=flag, run_if=run_if)
             self._decide()
-            ops.norm_modulate(self.x[n:], md[0], md[1], self.m[n:], eps, run_flag=flag, run_if=run_if)
-        else:
-            ops.norm_modulate(self.x, md[0], md[1], self.m, eps, run_flag=flag, run_if=run_if)
-        self._qkv_attention(p, p, flag, run_if)
-        ops.gemm(self.o, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=md[2], epilogue="gate_res",
+            if not askip:
+                ops.norm_modulate(self.x[n:], md[0], md[1], self.m[n:], eps, run_flag=aflag, run_if=arun)
+        elif not askip:
+            ops.norm_modulate(self.x, md[0], md[1], self.m, eps, run_flag=aflag, run_if=arun)
+        if not askip:
+            self._qkv_attention(p, p, aflag, arun)
+        ops.gemm(self._ob, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=md[2], epilogue="gate_res",
                  run_flag=flag, run_if=run_if)
         self._mlp(p, 0, R, md, flag, run_if)
 
-    def _block(self, i, flag, run_if, probe):
+    def _block(self, i, flag, run_if, probe, ag=None):
+        """Block i; ``ag`` = (skip, flag, run_if) of its attention part (attention-cache mode),
+        default: same gate as the block."""
         cfg = self.cfg
+        if ag is None:
+            ag = (False, flag, run_if)
+        self._bind_attention_output(i)
         if cfg.family == "single-dit":
-            return self._single_dit_block(i, flag, run_if, probe)
+            return self._single_dit_block(i, flag, run_if, probe, ag)
         if i < cfg.num_dual:
-            return self._mm_dual_block(i, flag, run_if, probe)
-        return self._mm_single_block(i - cfg.num_dual, flag, run_if, probe)
+            return self._mm_dual_block(i, flag, run_if, probe, ag)
+        return self._mm_single_block(i - cfg.num_dual, flag, run_if, probe, ag)
+
+    def _bind_attention_output(self, i):
+        """Where block i's attention output lives: the shared ``o`` buffer, or (attention-cache
+        mode) block i's cache slot, which a cached step reads instead of recomputing."""
+        if self.cache_mode == "attention-cache":
+            self._ob = self.ocache[i]
+            self._xo = self.xocache[i] if self.xocache is not None else None
+            if self.peer is not None:
+                g, H = self.geo, self.cfg.hidden_size
+                self._odst = self.peer_ocache.ptrs("ocache", (i * g.rows * H + self.sp.rank * self.hl *
+                                                               self.cfg.head_dim) * 2)
+        else:
+            self._ob, self._xo = self.o, self.o
+            if self.peer is not None:
+                self._odst = self.o_dst
+
+    def _alloc_attention_cache(self):
+        """Per-block attention-output slots [L, rows, H] (+ Single-DiT cross-attention [L, Sv_loc, H]).
+        Under the p2p Ulysses exchange the slots are peer memory (collective allocation)."""
+        if self.ocache is not None:
+            return
+        cfg, g, L, H = self.cfg, self.geo, self.cfg.num_layers, self.cfg.hidden_size
+        if self.peer is not None:
+            self.peer_ocache = PeerBuffers(self.sp, {"ocache": L * g.rows * H * 2}, self.device)
+            self.ocache = self.peer_ocache.local("ocache", (L, g.rows, H), BF16)
+        else:
+            self.ocache = torch.zeros(L, g.rows, H, device=self.device, dtype=self.act)
+        if cfg.family == "single-dit":
+            self.xocache = torch.zeros(L, g.Sv_loc, H, device=self.device, dtype=self.act)
 
     # ------------------------------------------------------------------ steps
-    def reset(self, x0: torch.Tensor, num_steps: int, policy=None):
-        """Load the initial latent [C, T, H, W] and the Euler grid t_i = i/N."""
+    def reset(self, x0: torch.Tensor, num_steps: int, policy=None, cache_mode: str = "dit-layer-cache"):
+        """Load the initial latent [C, T, H, W] and the Euler grid t_i = i/N.
+
+        ``cache_mode``: ``dit-layer-cache`` (rear-block offset reuse) or
+        ``attention-cache`` (per-block attention-output reuse)."""
         cfg, g = self.cfg, self.geo
         if g is None:
             raise ConfigError("call prepare() first", "model")
+        if cache_mode not in ("dit-layer-cache", "attention-cache"):
+            raise ConfigError("unknown cache mode", "cache.mode")
+        self.cache_mode = cache_mode
+        if cache_mode == "attention-cache":
+            self._alloc_attention_cache()
         C = cfg.latent_channels
         pt, ph, pw = cfg.patch
         exp = (C, g.grid[0] * pt, g.grid[1] * ph, g.grid[2] * pw)
@@ -489,6 +546,14 @@ class DiTModel:
         L, nf = cfg.num_layers, self.n_front
         dyn = mode == "dynamic"
         flag = self.flag if dyn else None
+        if self.cache_mode == "attention-cache":
+            # every block runs; only its attention part is skipped (static) or gated (dynamic)
+            self._embed()
+            ag = (mode == "cached", flag, 1)
+            for i in range(L):
+                self._block(i, None, 1, probe=(dyn and i == 0), ag=ag)
+            self._final()
+            return
         xi = self.x[:self.geo.Sv_loc]
         self._embed()
         cache = use_cache and nf < L

@@ -278,3 +278,22 @@ def unpatchify(tok, lat, grid, patch):
 def heads_to_seq(src, rows, P, width, dst, run_flag=None, run_if=1):
     _run("layout", 4 * rows * P * width, "aqb_heads_to_seq", _p(src), rows, P, width, _p(dst), dst.stride(0), _p(run_flag), int(run_if),
                  _stream())
+
+
+def tile_blend(ptrs, starts, counts, tile, overlap, latent, out):
+    """VAE tile blend (``aqb_tile_blend``); ptrs int64 / starts int32 device tensors."""
+    _need(out, F32, "tile_blend.out")
+    C = out.shape[0]
+    _run("layout", 8.0 * out.numel(), "aqb_tile_blend", _p(ptrs), _p(starts), *[int(c) for c in counts],
+         *[int(x) for x in tile], *[int(x) for x in overlap], *[int(x) for x in latent], C, _p(out), _stream())
+    return out
+
+
+def window_average(ptrs, starts, nclips, n, n_prime, out):
+    """Temporal MultiDiffusion Eq. 3 (``aqb_window_average``); out f32 [C, n', H, W]."""
+    _need(out, F32, "window_average.out")
+    C = out.shape[0]
+    hw = out[0, 0].numel()
+    _run("layout", 4.0 * out.numel() * (1 + n * nclips / n_prime), "aqb_window_average", _p(ptrs), _p(starts),
+         int(nclips), int(n), int(n_prime), C, hw, _p(out), _stream())
+    return out

@@ -39,7 +39,7 @@ class _Graphs:
         self.g = {}
 
     def run(self, model, mode, use_cache):
-        key = (id(model), model.generation, mode, use_cache, id(model.policy))
+        key = (id(model), model.generation, mode, use_cache, id(model.policy), model.cache_mode)
         if key not in self.g:
             # warm the kernels' one-time attribute setup outside capture
             s = torch.cuda.Stream()
@@ -73,9 +73,7 @@ def denoise(model, x0: torch.Tensor, num_steps: int, cache=None, trajectory: boo
             raise ConfigError("cache must be a CacheSchedule, a RelL1Policy or None", "sampler.cache")
         if cache.total_steps != num_steps:
             raise ConfigError("schedule length != num_steps", "sampler.cache")
-        if cache.mode != "dit-layer-cache" and not all(cache.per_step_full):
-            raise ConfigError("only dit-layer-cache is executable in this release", "cache.mode")
-    model.reset(x0, num_steps, policy=cache if dynamic else None)
+    model.reset(x0, num_steps, policy=cache if dynamic else None, cache_mode=cache.mode)
     use_cache = dynamic or not all(cache.per_step_full)
     traj = []
     if graph and graphs is None:

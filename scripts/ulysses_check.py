@@ -55,13 +55,14 @@ def run_cases(sp):
         inp = synthetic_inputs(cfg, grid)
         pooled = inp["pooled"] if cfg.family == "mm-dit" else None
         m_sp = build_model(cfg, weights=W, sp=sp).prepare(grid, inp["text"], pooled)
-        for cache in (plan_cache(8, warmup=2, interval=2), RelL1Policy(threshold=0.06, warmup=2)):
+        for cache in (plan_cache(8, warmup=2, interval=2), RelL1Policy(threshold=0.06, warmup=2),
+                      plan_cache(8, warmup=2, interval=2, mode="attention-cache")):
             r_sp = denoise(m_sp, inp["x0"], 8, cache, trajectory=True)
             if sp.rank == 0:
                 m1 = build_model(cfg, weights=W).prepare(grid, inp["text"], pooled)
                 r1 = denoise(m1, inp["x0"], 8, cache, trajectory=True)
                 orc = ref.OracleDiT(cfg, W, inp["text"], pooled, grid,
-                                    n_front=front_block_count(cfg.num_layers, 0.25))
+                                    n_front=front_block_count(cfg.num_layers, 0.25), mode=cache.mode)
                 if isinstance(cache, RelL1Policy):
                     lat, taken, _ = ref.denoise(orc, inp["x0"], 8, policy=cache)
                 else:
@@ -73,7 +74,7 @@ def run_cases(sp):
                 ok &= good
                 if m_sp.peer is not None and not m_sp.peer_ok():
                     good = False
-                print(json.dumps({"case": name, "P": P, "exchange": sp.exchange, "cache": type(cache).__name__,
+                print(json.dumps({"case": name, "P": P, "exchange": sp.exchange, "cache": f"{type(cache).__name__}/{cache.mode}",
                                   "schedule": r_sp.schedule.as_string(), "same_schedule": same,
                                   "max_rel_l2_vs_1gpu": e_sp_1, "max_rel_l2_vs_oracle": e_sp_o, "ok": good}),
                       flush=True)

@@ -167,3 +167,35 @@ def test_mmdit_13b_dims_two_blocks_match_oracle():
     res = denoise(model, inp["x0"], 2, None, trajectory=True)
     lat, _, _ = ref.denoise(orc, inp["x0"], 2, flags=[True, True])
     _check_traj(res, lat)
+
+
+@pytest.mark.parametrize("name", ["tiny-single", "single-d128", "mm-d128", "tiny-mm"])
+def test_attention_cache_mode_matches_oracle(name):
+    """attention-cache: cached steps reuse every block's attention output."""
+    cfg, grid = CASES[name]
+    steps = 4 if name.startswith("tiny") else 8
+    sched = plan_cache(steps, warmup=1, interval=2, mode="attention-cache")
+    model, _, inp = _setup(cfg, grid)
+    pooled = inp["pooled"] if cfg.family == "mm-dit" else None
+    orc = ref.OracleDiT(cfg, init_weights(cfg, seed=0), inp["text"], pooled, grid, mode="attention-cache")
+    res = denoise(model, inp["x0"], steps, sched, trajectory=True)
+    lat, taken, _ = ref.denoise(orc, inp["x0"], steps, flags=sched.per_step_full)
+    assert res.schedule.per_step_full == tuple(taken)
+    _check_traj(res, lat)
+    # graph replay of the same schedule is bit-identical
+    g = denoise(model, inp["x0"], steps, sched, graph=True).latent
+    assert torch.equal(g, res.latent)
+
+
+def test_attention_cache_mode_rel_l1_policy_and_fp32():
+    cfg, grid = CASES["single-d128"]
+    model, _, inp = _setup(cfg, grid, precision="fp32")
+    orc = ref.OracleDiT(cfg, init_weights(cfg, seed=0), inp["text"], None, grid, mode="attention-cache")
+    _, _, probe = ref.denoise(orc, inp["x0"], 4, policy=RelL1Policy(threshold=1e9, warmup=1))
+    thr = 2.5 * sorted(probe[1:])[len(probe[1:]) // 2]
+    pol = RelL1Policy(threshold=thr, warmup=2, mode="attention-cache")
+    lat, taken, _ = ref.denoise(orc, inp["x0"], 10, policy=pol)
+    assert 0 < taken.count(False)
+    res = denoise(model, inp["x0"], 10, pol, trajectory=True)
+    assert list(res.schedule.per_step_full) == taken
+    _check_traj(res, lat, tol=TOL_FP32)
