@@ -193,14 +193,17 @@ int aqb_cache_offset(float* x, int64_t ldx, float* off, int64_t rows, int32_t hi
 int aqb_step_scalars(const float* ts, const float* dts, int32_t* idx, float* cur, int32_t mode, void* stream);
 
 /* ---------------------------------------------------------------------------
- * Latent layout: lat f32 [C, T*pt, H*ph, W*pw]  <->  tokens [T*H*W, pt*ph*pw*C]
+ * Latent layout: lat f32 [C, lat_frames, H*ph, W*pw] whose frames
+ * [frame_offset, frame_offset + T*pt)  <->  tokens [T*H*W, pt*ph*pw*C]
  * (token-major, features ordered (pt, ph, pw, c)).  patchify writes f32 tokens
- * and a bf16 copy (tok_bf16 may be NULL); unpatchify reads f32 tokens.
+ * and a bf16 copy (tok_bf16 may be NULL); unpatchify reads f32 tokens.  The
+ * frame window serves temporal MultiDiffusion clips of a longer latent
+ * (PAPER.md:411); lat_frames = T*pt, frame_offset = 0 for a whole latent.
  */
 int aqb_patchify(const float* lat, float* tok, void* tok_bf16, int32_t C, int32_t T, int32_t H, int32_t W,
-                 int32_t pt, int32_t ph, int32_t pw, void* stream);
+                 int32_t pt, int32_t ph, int32_t pw, int32_t lat_frames, int32_t frame_offset, void* stream);
 int aqb_unpatchify(const float* tok, float* lat, int32_t C, int32_t T, int32_t H, int32_t W, int32_t pt,
-                   int32_t ph, int32_t pw, void* stream);
+                   int32_t ph, int32_t pw, int32_t lat_frames, int32_t frame_offset, void* stream);
 
 /* Ulysses head->sequence repack: src bf16 [P, rows, hpg*D] -> dst [rows, P*hpg*D] (row stride ld_dst). */
 int aqb_heads_to_seq(const void* src, int64_t rows, int32_t P, int32_t width, void* dst, int64_t ld_dst,

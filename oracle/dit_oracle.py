@@ -367,3 +367,33 @@ def _probe(model: OracleDiT, x_tok, t):
     else:
         mi = linear(W, "single.0.mod", silu(vec)).reshape(6, H)
     return modulate(img, mi[0], mi[1], cfg.norm_eps), None
+
+
+def denoise_windows(models, x0_lat: torch.Tensor, num_steps: int, clips, flags=None):
+    """Temporal MultiDiffusion (Eq. 3) — fp32 restatement.
+
+    ``models[k]`` is an :class:`OracleDiT` for clip ``k`` (clip geometry; each keeps its
+    own cache state), ``clips`` the WindowPlan's ``(start, end)`` latent-frame ranges.
+    Every step each clip ``x'[:, s:e]`` takes one Euler step; frame ``i`` then becomes
+    the mean over the clips covering it (sum in clip order / |S(i)|).  Returns the latent
+    after every step (``num_steps + 1`` entries).
+    """
+    cfg = models[0].cfg
+    x = x0_lat.to(f32).clone()
+    states = [{} for _ in clips]
+    out = [x.clone()]
+    count = torch.zeros(x.shape[1])
+    for s, e in clips:
+        count[s:e] += 1
+    for i in range(num_steps):
+        t = i / num_steps
+        full = True if flags is None else bool(flags[i])
+        acc = torch.zeros_like(x)
+        for (s, e), m, st in zip(clips, models, states):
+            tok = patchify(x[:, s:e], cfg.patch)
+            v, _ = m.velocity(tok, t, full=full, state=st)
+            tok = tok + (1.0 / num_steps) * v
+            acc[:, s:e] += unpatchify(tok, m.grid, cfg.patch, cfg.latent_channels)
+        x = acc / count[None, :, None, None]
+        out.append(x.clone())
+    return out

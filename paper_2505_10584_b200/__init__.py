@@ -6,9 +6,11 @@ Public API (drop-in for the reference's cache-schedule boundary,
 * ``plan_cache``, ``CacheSchedule``, ``CACHE_MODES``,
   ``DEFAULT_CACHED_COST_FRACTION``, ``dit_parallel_latency``,
   ``composite_speedup``, ``ConfigError``, ``PlanningError``, ``DimensionError``
+* ``plan_vae_tiles`` / ``TilePlan`` / ``Tile`` and ``plan_temporal_windows`` /
+  ``WindowPlan`` (``inference.py:89-279``), with GPU blend / Eq. 3 kernels
 * new: ``RelL1Policy``, ``DiTConfig`` + presets, ``SingleDiT`` / ``MMDiT``
-  (model construction), ``denoise`` (sampler loop), ``latent_shape``,
-  ``token_count``.
+  (model construction), ``denoise`` (sampler loop), ``denoise_windows``
+  (temporal MultiDiffusion), ``latent_shape``, ``token_count``.
 
 The model/sampler symbols need CUDA and ``libaqb.so`` (hand-written sm_100a
 kernels); they are imported lazily so the schedule API works anywhere.
@@ -40,6 +42,8 @@ from .schedule import (
     plan_cache,
 )
 
+from .tiling import Tile, TilePlan, WindowPlan, plan_temporal_windows, plan_vae_tiles
+
 __version__ = "0.1.0"
 
 _LAZY = {
@@ -48,6 +52,7 @@ _LAZY = {
     "build_model": ("model", "build_model"),
     "denoise": ("sampler", "denoise"),
     "DenoiseResult": ("sampler", "DenoiseResult"),
+    "denoise_windows": ("sampler", "denoise_windows"),
 }
 
 
@@ -65,5 +70,6 @@ __all__ = [
     "DiTConfig", "MM_DIT_13B", "NativeError", "PRESETS", "PlanningError", "RelL1Policy", "SINGLE_DIT_2B",
     "TINY_MM", "TINY_SINGLE", "VaeSpec", "VideoSpec", "composite_speedup", "dit_parallel_latency",
     "flops_per_step", "front_block_count", "latent_shape", "no_cache", "plan_cache", "token_count",
-    "SingleDiT", "MMDiT", "build_model", "denoise", "DenoiseResult",
+    "SingleDiT", "MMDiT", "build_model", "denoise", "DenoiseResult", "denoise_windows",
+    "Tile", "TilePlan", "WindowPlan", "plan_vae_tiles", "plan_temporal_windows",
 ]

@@ -64,8 +64,10 @@ SIGNATURES = {
     "aqb_cache_decide": (c_int, [P, P, c_float, c_int32, c_int32, c_int32, P, P, P]),
     "aqb_cache_offset": (c_int, [P, c_int64, P, c_int64, c_int32, c_int32, P, c_int32, P]),
     "aqb_step_scalars": (c_int, [P, P, P, P, c_int32, P]),
-    "aqb_patchify": (c_int, [P, P, P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, P]),
-    "aqb_unpatchify": (c_int, [P, P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, P]),
+    "aqb_patchify": (c_int, [P, P, P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
+                             P]),
+    "aqb_unpatchify": (c_int, [P, P, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32, c_int32,
+                               P]),
     "aqb_heads_to_seq": (c_int, [P, c_int64, c_int32, c_int32, P, c_int64, P, c_int32, P]),
 }
 

@@ -9,7 +9,7 @@
 // tensor core always has the other tile's work while one tile's softmax runs).
 //   warp 0      TMA producer: Q0, Q1 once; K_j, V_j through an NS-deep ring.
 //   warp 1      MMA issuer (one thread):  S_t = Q_t K_j^T  (SS, M=128 N=128)
-//               O_t += P_t V_j  (P from smem K-major, V MN-major, N=D).
+//               O_t += P_t V_j  (P from TMEM — the TS form — V MN-major, N=D).
 //   warps 4-7   softmax of tile 0, warps 8-11 softmax of tile 1: thread = query
 //               row (TMEM lane), 224 registers each (setmaxnreg).  Online
 //               softmax in the exp2 domain: scale folded into one packed
@@ -17,9 +17,11 @@
 //               degree-3 polynomial on the FMA pipe (the rest on MUFU) so
 //               neither pipe caps the tensor core; lazy rescaling (only when
 //               the running max grows by > 8, so O in TMEM is rarely
-//               touched); P written with st.shared.v4 in the 128B-swizzled
-//               K-major layout the MMA reads; final 1/l normalisation and
-//               bf16 store from the same warps.
+//               touched); P written back to TMEM as packed bf16 pairs over
+//               the consumed half of S_t (tcgen05.st), so the PV MMA reads A
+//               from TMEM and only V from shared memory (smem operand traffic
+//               per KV block drops from 160 KB to 96 KB per Q tile); final
+//               1/l normalisation and TMA-staged bf16 store from the same warps.
 // TMEM: S0 | S1 | O0 | O1  (128 + 128 + D + D columns).
 #include <algorithm>
 #include <cmath>
@@ -36,18 +38,17 @@ constexpr int BKV = 128;  // keys per KV tile (MMA N of QK^T, K of PV)
 constexpr int kThreads = 384;    // 3 warpgroups: control | softmax tile 0 | softmax tile 1
 constexpr uint32_t kCtrlRegs = 56;     // setmaxnreg budgets: 56 + 2 * 224 <= 512 per SMSP
 constexpr uint32_t kSoftmaxRegs = 224;
-constexpr uint32_t kPolyMask = 0x52;   // pairs (i & 7) in {1,4,6}: exp2 by polynomial (3/8 off the MUFU)
+constexpr uint32_t kPolyMask = 0x52;
+constexpr uint32_t kPCol = 64;         // P_t (bf16 pairs) lives in columns 64..127 of S_t   // pairs (i & 7) in {1,4,6}: exp2 by polynomial (3/8 off the MUFU)
 
 template <int D>
 struct Cfg {
-  static constexpr int NS = D == 128 ? 3 : 4;                // K/V ring depth
+  static constexpr int NS = D == 128 ? 5 : 6;                // K/V ring depth
   static constexpr int kQBytes = BQ * D * 2;                 // one Q tile
   static constexpr int kKVBytes = BKV * D * 2;               // one K or V tile
-  static constexpr int kPBytes = BQ * BKV * 2;               // one P tile
   static constexpr int kOffQ = 0;
   static constexpr int kOffKV = 2 * kQBytes;
-  static constexpr int kOffP = kOffKV + NS * kKVBytes;
-  static constexpr int kOffBar = kOffP + 2 * kPBytes;
+  static constexpr int kOffBar = kOffKV + NS * kKVBytes;
   static constexpr int kSmem = kOffBar + 256 + 1024;
   static constexpr int kBoxes = D / 64;                      // 64-column TMA boxes per row
 };
@@ -116,7 +117,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = base + C::kOffQ;
   uint8_t* sKV = base + C::kOffKV;
-  uint8_t* sP = base + C::kOffP;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::kOffBar);
   uint64_t* q_full = bars;              // 1
   uint64_t* kv_full = bars + 1;         // NS
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (lane == 0) {
       constexpr uint32_t kIdescS = idesc_bf16(BQ, BKV, 0, 0);  // Q, K both K-major
       constexpr uint32_t kIdescO = idesc_bf16(BQ, D, 0, 1);    // P K-major, V MN-major
-      const uint32_t q_addr = smem_u32(sQ), kv_addr = smem_u32(sKV), p_addr = smem_u32(sP);
+      const uint32_t q_addr = smem_u32(sQ), kv_addr = smem_u32(sKV);
       auto issue_qk = [&](int t, int stage) {
         const uint32_t a0 = q_addr + t * C::kQBytes, b0 = kv_addr + stage * C::kKVBytes;
 #pragma unroll
@@ -190,13 +190,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       };
       auto issue_pv = [&](int t, int stage, bool acc) {
-        const uint32_t a0 = p_addr + t * C::kPBytes, b0 = kv_addr + stage * C::kKVBytes;
+        // A = P_t straight from TMEM (columns 64..127 of S_t, bf16 pairs), B = V (MN-major smem)
+        const uint32_t a0 = tmem + t * 128 + kPCol, b0 = kv_addr + stage * C::kKVBytes;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
-          const uint32_t aoff = (kk >> 2) * (BQ * 128) + (kk & 3) * 32;
           const uint32_t boff = kk * 16 * 128;  // 16 keys x 128 B rows
-          umma_bf16_ss(tmem + 256 + t * D, smem_desc(a0 + aoff, 0, 1024), smem_desc(b0 + boff, BKV * 128, 1024),
-                       kIdescO, (acc || kk > 0) ? 1u : 0u);
+          umma_bf16_ts(tmem + 256 + t * D, a0 + kk * 8, smem_desc(b0 + boff, BKV * 128, 1024), kIdescO,
+                       (acc || kk > 0) ? 1u : 0u);
         }
       };
       mbar_wait(q_full, 0);
@@ -241,7 +241,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t lane_base = (quad * 32) << 16;
     const uint32_t s_tmem = tmem + lane_base + t * 128;
     const uint32_t o_tmem = tmem + lane_base + 256 + t * D;
-    const uint32_t prow = smem_u32(sP + t * C::kPBytes + r * 128);
     const uint32_t sw = r & 7;
     const float c = p.scale_log2;
     const uint64_t c2 = f2pack(c, c);
@@ -295,9 +294,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float nm = -m_run * c;
       const uint64_t nm2 = f2pack(nm, nm);
       uint64_t acc2 = f2pack(0.f, 0.f);
+      uint32_t pp[16];  // 16 packed bf16 pairs = 16 TMEM columns, stored as they fill
 #pragma unroll
-      for (int kc = 0; kc < BKV / 8; ++kc) {  // 16-byte chunks of the P row
-        uint32_t pk[4];
+      for (int kc = 0; kc < BKV / 8; ++kc) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int pi = kc * 4 + q;
@@ -309,11 +308,11 @@ __global__ void __launch_bounds__(kThreads, 1)
             const uint64_t xc = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
             const uint64_t tt = fadd2(xc, kM);
             const uint64_t fr = fsub2(xc, fsub2(tt, kM));
-            uint64_t pp = ffma2(fr, kC3, kC2);
-            pp = ffma2(pp, fr, kC1);
-            pp = ffma2(pp, fr, kC0);
+            uint64_t pq = ffma2(fr, kC3, kC2);
+            pq = ffma2(pq, fr, kC1);
+            pq = ffma2(pq, fr, kC0);
             float q0, q1, t0, t1;
-            f2unpack(pp, q0, q1);
+            f2unpack(pq, q0, q1);
             f2unpack(tt, t0, t1);
             p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
             p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
@@ -322,15 +321,14 @@ __global__ void __launch_bounds__(kThreads, 1)
             p1 = ex2(x1);
           }
           acc2 = fadd2(acc2, f2pack(p0, p1));
-          pk[q] = pack_bf16(p0, p1);
+          pp[(kc & 3) * 4 + q] = pack_bf16(p0, p1);
         }
-        const int box = kc >> 3, cch = kc & 7;
-        st_shared_v4(prow + box * (BQ * 128) + ((cch ^ sw) << 4), pk[0], pk[1], pk[2], pk[3]);
+        if ((kc & 3) == 3) tmem_st16(s_tmem + kPCol + (kc >> 2) * 16, pp);
       }
       float a0, a1;
       f2unpack(acc2, a0, a1);
       l_run += a0 + a1;
-      fence_proxy_async_smem();  // generic-proxy P stores -> visible to the tensor core
+      tmem_wait_st();  // P in TMEM before the MMA warp may read it
       tc_fence_before();
       mbar_arrive(p_full + t);
     }
@@ -363,43 +361,53 @@ __global__ void __launch_bounds__(kThreads, 1)
       // and under the Ulysses scatter straight into the owning ranks' buffers.
       uint8_t* stile = sQ + t * C::kQBytes;
       const uint32_t srow = smem_u32(stile) + r * 128;
+      const OutMap& m = p.out;
+      const int tr0 = q0 + t * BQ;  // first row of this tile
+      // TMA coordinates must be >= 0: a tile that starts in one rank's rows and ends in
+      // the next (or in the text rows) is written with direct stores instead.
+      const int64_t last = min(int64_t(tr0 + BQ - 1), int64_t(p.seq_q - 1));
+      const bool use_tma = m.nranks == 0 || tr0 >= m.text_row0 ||
+                           (last < m.text_row0 && tr0 / m.rows_per_rank == last / m.rows_per_rank);
 #pragma unroll 1
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t u[32];
         tmem_ld32(o_tmem + cc * 32, u);
         tmem_wait_ld();
-        const uint32_t bx = srow + (cc >> 1) * (BQ * 128);
+        uint4 pk[4];
 #pragma unroll
         for (int g = 0; g < 4; ++g)
-          st_shared_v4(bx + ((((cc & 1) * 4 + g) ^ sw) << 4),
-                       pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
-                       pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
-                       pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
-                       pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
-      }
-      fence_proxy_async_smem();
-      named_bar_sync(1 + t, 128);
-      if (quad == 0 && lane == 0) {
-        const int tr0 = q0 + t * BQ;  // first row of this tile
-        const OutMap& m = p.out;
-        for (int c = 0; c < C::kBoxes; ++c) {
-          const uint8_t* src = stile + c * (BQ * 128);
-          if (m.nranks == 0) {
-            tma_store_3d(&om.local, src, c * 64, head, tr0);
-          } else {
-            const int64_t vend = (tr0 + BQ < m.text_row0) ? int64_t(tr0 + BQ) : m.text_row0;
-            if (tr0 < vend) {
-              const int r0 = int(tr0 / m.rows_per_rank), r1 = int((vend - 1) / m.rows_per_rank);
-              for (int rr = r0; rr <= r1; ++rr)
-                tma_store_3d(&om.vid[rr], src, c * 64, head, int(tr0 - rr * m.rows_per_rank));
-            }
-            if (tr0 + BQ > m.text_row0)
-              for (int rr = 0; rr < m.nranks; ++rr)
-                tma_store_3d(&om.txt[rr], src, c * 64, head, int(tr0 - m.text_row0));
-          }
+          pk[g] = make_uint4(pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
+                             pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
+                             pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
+                             pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
+        if (use_tma) {
+          const uint32_t bx = srow + (cc >> 1) * (BQ * 128);
+#pragma unroll
+          for (int g = 0; g < 4; ++g)
+            st_shared_v4(bx + ((((cc & 1) * 4 + g) ^ sw) << 4), pk[g].x, pk[g].y, pk[g].z, pk[g].w);
+        } else if (live && cc * 32 < p.head_dim) {
+          for_each_out(m, head, row, [&](__nv_bfloat16* orow) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = pk[g];
+          });
         }
-        bulk_commit();
-        bulk_wait<0>();  // complete (not just read out of smem) before the CTA exits
+      }
+      if (use_tma) {
+        fence_proxy_async_smem();
+        named_bar_sync(1 + t, 128);
+        if (quad == 0 && lane == 0) {
+          for (int c = 0; c < C::kBoxes; ++c) {
+            const uint8_t* src = stile + c * (BQ * 128);
+            if (m.nranks == 0)
+              tma_store_3d(&om.local, src, c * 64, head, tr0);
+            else if (tr0 >= m.text_row0)
+              for (int rr = 0; rr < m.nranks; ++rr) tma_store_3d(&om.txt[rr], src, c * 64, head, int(tr0 - m.text_row0));
+            else
+              tma_store_3d(&om.vid[tr0 / m.rows_per_rank], src, c * 64, head, int(tr0 % m.rows_per_rank));
+          }
+          bulk_commit();
+          bulk_wait<0>();  // complete (not just read out of smem) before the CTA exits
+        }
       }
     }
   } else {

@@ -291,8 +291,10 @@ __global__ void step_scalars_kernel(const float* ts, const float* dts, int32_t* 
 }
 
 // ----------------------------------------------------------- latent layout
+// lat is [C, Tl, H*ph, W*pw]; the T*pt frames starting at frame t0 are (un)patchified
+// (a temporal window of a longer latent: MultiDiffusion clips).
 __global__ void patchify_kernel(const float* lat, float* tok, __nv_bfloat16* tokb, int C, int T, int H, int W, int pt,
-                                int ph, int pw) {
+                                int ph, int pw, int Tl, int t0) {
   const int F = pt * ph * pw * C;
   const int64_t n = static_cast<int64_t>(T) * H * W * F;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -306,13 +308,14 @@ __global__ void patchify_kernel(const float* lat, float* tok, __nv_bfloat16* tok
     const int ih = f % ph;
     const int it = f / ph;
     const int w = static_cast<int>(s % W), h = static_cast<int>((s / W) % H), t = static_cast<int>(s / (W * H));
-    const float v = lat[((static_cast<int64_t>(c) * T * pt + t * pt + it) * H * ph + h * ph + ih) * W * pw + w * pw + iw];
+    const float v = lat[((static_cast<int64_t>(c) * Tl + t0 + t * pt + it) * H * ph + h * ph + ih) * W * pw + w * pw + iw];
     tok[i] = v;
     if (tokb) tokb[i] = __float2bfloat16(v);
   }
 }
 
-__global__ void unpatchify_kernel(const float* tok, float* lat, int C, int T, int H, int W, int pt, int ph, int pw) {
+__global__ void unpatchify_kernel(const float* tok, float* lat, int C, int T, int H, int W, int pt, int ph, int pw,
+                                  int Tl, int t0) {
   const int F = pt * ph * pw * C;
   const int64_t n = static_cast<int64_t>(T) * H * W * F;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -326,7 +329,7 @@ __global__ void unpatchify_kernel(const float* tok, float* lat, int C, int T, in
     const int ih = f % ph;
     const int it = f / ph;
     const int w = static_cast<int>(s % W), h = static_cast<int>((s / W) % H), t = static_cast<int>(s / (W * H));
-    lat[((static_cast<int64_t>(c) * T * pt + t * pt + it) * H * ph + h * ph + ih) * W * pw + w * pw + iw] = tok[i];
+    lat[((static_cast<int64_t>(c) * Tl + t0 + t * pt + it) * H * ph + h * ph + ih) * W * pw + w * pw + iw] = tok[i];
   }
 }
 
@@ -519,21 +522,25 @@ extern "C" int aqb_step_scalars(const float* ts, const float* dts, int32_t* idx,
 }
 
 extern "C" int aqb_patchify(const float* lat, float* tok, void* tok_bf16, int32_t C, int32_t T, int32_t H, int32_t W,
-                            int32_t pt, int32_t ph, int32_t pw, void* stream) {
+                            int32_t pt, int32_t ph, int32_t pw, int32_t lat_frames, int32_t frame_offset,
+                            void* stream) {
   AQB_CHECK_ARG(lat && tok && C > 0 && T > 0 && H > 0 && W > 0 && pt > 0 && ph > 0 && pw > 0, "patchify: bad args");
+  AQB_CHECK_ARG(frame_offset >= 0 && frame_offset + T * pt <= lat_frames, "patchify: frame window out of range");
   const int64_t n = static_cast<int64_t>(C) * T * H * W * pt * ph * pw;
   patchify_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      lat, tok, reinterpret_cast<__nv_bfloat16*>(tok_bf16), C, T, H, W, pt, ph, pw);
+      lat, tok, reinterpret_cast<__nv_bfloat16*>(tok_bf16), C, T, H, W, pt, ph, pw, lat_frames, frame_offset);
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
 
 extern "C" int aqb_unpatchify(const float* tok, float* lat, int32_t C, int32_t T, int32_t H, int32_t W, int32_t pt,
-                              int32_t ph, int32_t pw, void* stream) {
+                              int32_t ph, int32_t pw, int32_t lat_frames, int32_t frame_offset, void* stream) {
   AQB_CHECK_ARG(lat && tok && C > 0 && T > 0 && H > 0 && W > 0 && pt > 0 && ph > 0 && pw > 0, "unpatchify: bad args");
+  AQB_CHECK_ARG(frame_offset >= 0 && frame_offset + T * pt <= lat_frames, "unpatchify: frame window out of range");
   const int64_t n = static_cast<int64_t>(C) * T * H * W * pt * ph * pw;
   unpatchify_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(tok, lat, C, T, H, W, pt,
-                                                                                           ph, pw);
+                                                                                           ph, pw, lat_frames,
+                                                                                           frame_offset);
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }

@@ -122,6 +122,7 @@ class DiTModel:
     def prepare(self, grid, text: torch.Tensor, pooled: torch.Tensor | None = None):
         """Bind geometry + conditioning; allocate the step workspace."""
         cfg, dev = self.cfg, self.device
+        self._text, self._pooled = text, pooled
         grid = tuple(int(g) for g in grid)
         Sv = grid[0] * grid[1] * grid[2]
         P = 1 if self.sp is None else self.sp.P
@@ -452,11 +453,14 @@ class DiTModel:
             self.xocache = torch.zeros(L, g.Sv_loc, H, device=self.device, dtype=self.act)
 
     # ------------------------------------------------------------------ steps
-    def reset(self, x0: torch.Tensor, num_steps: int, policy=None, cache_mode: str = "dit-layer-cache"):
+    def reset(self, x0: torch.Tensor, num_steps: int, policy=None, cache_mode: str = "dit-layer-cache",
+              frame_offset: int | None = None):
         """Load the initial latent [C, T, H, W] and the Euler grid t_i = i/N.
 
         ``cache_mode``: ``dit-layer-cache`` (rear-block offset reuse) or
-        ``attention-cache`` (per-block attention-output reuse)."""
+        ``attention-cache`` (per-block attention-output reuse).
+        ``frame_offset``: ``x0`` is a longer latent and this model's clip starts at that
+        latent frame (temporal MultiDiffusion)."""
         cfg, g = self.cfg, self.geo
         if g is None:
             raise ConfigError("call prepare() first", "model")
@@ -468,15 +472,15 @@ class DiTModel:
         C = cfg.latent_channels
         pt, ph, pw = cfg.patch
         exp = (C, g.grid[0] * pt, g.grid[1] * ph, g.grid[2] * pw)
-        if tuple(x0.shape) != exp:
-            raise ConfigError(f"latent must be {exp}, got {tuple(x0.shape)}", "inputs.x0")
+        shape = tuple(x0.shape)
+        if frame_offset is None:
+            if shape != exp:
+                raise ConfigError(f"latent must be {exp}, got {shape}", "inputs.x0")
+        elif (len(shape) != 4 or shape[0] != C or shape[2:] != exp[2:] or frame_offset < 0
+              or frame_offset + exp[1] > shape[1]):
+            raise ConfigError(f"clip {exp} at frame {frame_offset} does not fit latent {shape}", "inputs.x0")
         dev = self.device
-        full_tok = torch.empty(g.Sv, cfg.patch_dim, device=dev, dtype=F32)
-        lat = x0.to(dev, F32, non_blocking=True).contiguous()
-        ops.patchify(lat, full_tok, None, g.grid, cfg.patch)
-        r = 0 if self.sp is None else self.sp.rank
-        self.lat.copy_(full_tok[r * g.Sv_loc:(r + 1) * g.Sv_loc])
-        self.lat_bf.copy_(self.lat)
+        self.load_latent(x0.to(dev, F32, non_blocking=True).contiguous(), frame_offset or 0)
         if getattr(self, "num_steps", None) != num_steps:
             # (re)allocate the per-step tables; captured CUDA graphs hold their addresses,
             # so a new step count starts a new graph generation
@@ -494,6 +498,34 @@ class DiTModel:
         self.cstate.zero_()
         self.prev.zero_()
         self.policy = policy
+
+    def load_latent(self, lat: torch.Tensor, frame_offset: int = 0):
+        """Set the denoise state from latent frames [frame_offset, +T*pt) of ``lat`` (f32
+        [C, Tl, H, W] on this device) — one patchify kernel (+ this rank's token slice)."""
+        cfg, g = self.cfg, self.geo
+        if self.sp is None or self.sp.P == 1:
+            ops.patchify(lat, self.lat, self.lat_bf if not self.fp32 else None, g.grid, cfg.patch, frame_offset)
+            if self.fp32:
+                self.lat_bf.copy_(self.lat)
+            return
+        full_tok = torch.empty(g.Sv, cfg.patch_dim, device=self.device, dtype=F32)
+        ops.patchify(lat, full_tok, None, g.grid, cfg.patch, frame_offset)
+        r = self.sp.rank
+        self.lat.copy_(full_tok[r * g.Sv_loc:(r + 1) * g.Sv_loc])
+        self.lat_bf.copy_(self.lat)
+
+    def fork(self):
+        """A second denoise context sharing this model's weights (its own activations, cache
+        state and step tables) — one per temporal-MultiDiffusion clip."""
+        import copy
+
+        if self.geo is None:
+            raise ConfigError("call prepare() first", "model")
+        twin = copy.copy(self)
+        for a in ("num_steps", "ts", "dts", "flags_out", "rels_out", "peer_ocache"):
+            twin.__dict__.pop(a, None)
+        twin.generation = 0
+        return twin.prepare(self.geo.grid, self._text, self._pooled)
 
     def _decide(self):
         pol = self.policy
@@ -571,8 +603,8 @@ class DiTModel:
             ops.cache_offset(xi, self.off, 1, run_flag=flag, run_if=1)
         self._final()
 
-    def latent(self) -> torch.Tensor:
-        """Current latent [C, T, H, W] (gathered over Ulysses ranks)."""
+    def latent(self, out: torch.Tensor | None = None) -> torch.Tensor:
+        """Current latent [C, T, H, W] (gathered over Ulysses ranks), optionally into ``out``."""
         cfg, g = self.cfg, self.geo
         tok = self.lat
         if self.sp is not None and self.sp.P > 1:
@@ -580,8 +612,9 @@ class DiTModel:
             self.sp.all_gather(full.view(-1), self.lat.view(-1))
             tok = full
         pt, ph, pw = cfg.patch
-        out = torch.empty(cfg.latent_channels, g.grid[0] * pt, g.grid[1] * ph, g.grid[2] * pw, device=self.device,
-                          dtype=F32)
+        if out is None:
+            out = torch.empty(cfg.latent_channels, g.grid[0] * pt, g.grid[1] * ph, g.grid[2] * pw,
+                              device=self.device, dtype=F32)
         ops.unpatchify(tok, out, g.grid, cfg.patch)
         return out
 

@@ -263,16 +263,17 @@ def step_scalars(ts, dts, idx, cur, advance=False):
     _run("small", 0, "aqb_step_scalars", _p(ts), _p(dts), _p(idx), _p(cur), int(bool(advance)), _stream())
 
 
-def patchify(lat, tok, tok_bf16, grid, patch):
-    C = lat.shape[0]
-    _run("layout", 10 * lat.numel(), "aqb_patchify", _p(lat), _p(tok), _p(tok_bf16), C, grid[0], grid[1], grid[2], patch[0], patch[1],
-                 patch[2], _stream())
+def patchify(lat, tok, tok_bf16, grid, patch, frame_offset=0):
+    """tokens <- latent frames [frame_offset, frame_offset + T*pt) of lat [C, Tl, H, W]."""
+    C, Tl = lat.shape[0], lat.shape[1]
+    _run("layout", 10 * tok.numel(), "aqb_patchify", _p(lat), _p(tok), _p(tok_bf16), C, grid[0], grid[1], grid[2],
+         patch[0], patch[1], patch[2], Tl, int(frame_offset), _stream())
 
 
-def unpatchify(tok, lat, grid, patch):
-    C = lat.shape[0]
-    _run("layout", 8 * lat.numel(), "aqb_unpatchify", _p(tok), _p(lat), C, grid[0], grid[1], grid[2], patch[0], patch[1], patch[2],
-                 _stream())
+def unpatchify(tok, lat, grid, patch, frame_offset=0):
+    C, Tl = lat.shape[0], lat.shape[1]
+    _run("layout", 8 * tok.numel(), "aqb_unpatchify", _p(tok), _p(lat), C, grid[0], grid[1], grid[2], patch[0],
+         patch[1], patch[2], Tl, int(frame_offset), _stream())
 
 
 def heads_to_seq(src, rows, P, width, dst, run_flag=None, run_if=1):

@@ -94,3 +94,67 @@ def denoise(model, x0: torch.Tensor, num_steps: int, cache=None, trajectory: boo
     else:
         sched, rels = cache, []
     return DenoiseResult(latent=lat, schedule=sched, rel_l1=rels, trajectory=traj)
+
+
+@dataclass
+class WindowDenoiseResult:
+    latent: torch.Tensor                  # [C, n', H, W] f32 (device)
+    schedules: list                       # per clip: flags actually taken
+    trajectory: list = field(default_factory=list)
+
+
+def denoise_windows(model, x0: torch.Tensor, num_steps: int, plan, cache=None, trajectory: bool = False,
+                    graph: bool = False) -> WindowDenoiseResult:
+    """Temporal MultiDiffusion around the denoise step.
+
+    ``plan``: a :class:`~paper_2505_10584_b200.tiling.WindowPlan` over the latent's
+    frames (``n' = x0.shape[1]``, window ``n`` = the model's clip frames).  Every step,
+    each clip ``x'[s_k : s_k + n]`` runs one denoise step (velocity + Euler, with its own
+    diffusion-cache state) and Eq. 3 averages the clips back into ``x'`` on the GPU
+    (``aqb_window_average``); the next step starts from the averaged latent.
+    ``model`` must be prepared for the clip geometry; the other clips get
+    :meth:`DiTModel.fork` contexts sharing its weights.
+    """
+    from .tiling import average_windows
+
+    if num_steps < 1:
+        raise ConfigError("num_steps must be >= 1", "sampler.num_steps")
+    if cache is None:
+        cache = no_cache(num_steps)
+    dynamic = isinstance(cache, RelL1Policy)
+    if not dynamic and (not isinstance(cache, CacheSchedule) or cache.total_steps != num_steps):
+        raise ConfigError("cache must be a CacheSchedule of num_steps steps, a RelL1Policy or None", "sampler.cache")
+    g, cfg = model.geo, model.cfg
+    pt = cfg.patch[0]
+    if g is None:
+        raise ConfigError("call prepare() first", "model")
+    if plan.window != g.grid[0] * pt or plan.n_prime != x0.shape[1]:
+        raise ConfigError(f"window {plan.window} / latent {x0.shape[1]} frames vs model clip {g.grid[0] * pt}",
+                          "windows")
+    dev = model.device
+    x = x0.to(dev, torch.float32).contiguous().clone()
+    ctxs = [model] + [model.fork() for _ in range(plan.num_clips - 1)]
+    for ctx, (s0, _) in zip(ctxs, plan.clips):
+        ctx.reset(x, num_steps, policy=cache if dynamic else None, cache_mode=cache.mode, frame_offset=s0)
+    clips = [torch.empty(cfg.latent_channels, plan.window, *x.shape[2:], device=dev) for _ in plan.clips]
+    use_cache = dynamic or not all(cache.per_step_full)
+    graphs = _Graphs() if graph else None
+    traj = []
+    for i in range(num_steps):
+        mode = "dynamic" if dynamic else ("full" if cache.per_step_full[i] else "cached")
+        for k, (ctx, (s0, _)) in enumerate(zip(ctxs, plan.clips)):
+            if i > 0:
+                ctx.load_latent(x, s0)
+            if graph:
+                graphs.run(ctx, mode, use_cache)
+            else:
+                ctx.step(mode, use_cache)
+            ctx.latent(out=clips[k])
+        average_windows(plan, clips, x)
+        if trajectory:
+            traj.append(x.clone())
+    if dynamic:
+        scheds = [cache.as_schedule([bool(f) for f in c.flags_out.tolist()]) for c in ctxs]
+    else:
+        scheds = [cache] * len(ctxs)
+    return WindowDenoiseResult(latent=x, schedules=scheds, trajectory=traj)

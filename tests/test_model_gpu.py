@@ -199,3 +199,27 @@ def test_attention_cache_mode_rel_l1_policy_and_fp32():
     res = denoise(model, inp["x0"], 10, pol, trajectory=True)
     assert list(res.schedule.per_step_full) == taken
     _check_traj(res, lat, tol=TOL_FP32)
+
+
+@pytest.mark.parametrize("name,n_prime,window,stride", [("tiny-single", 6, 4, 2), ("mm-d128", 9, 3, 2)])
+def test_temporal_multidiffusion_matches_oracle(name, n_prime, window, stride):
+    """denoise_windows: per-clip Euler steps + Eq. 3 averaging on the GPU vs the fp32 oracle."""
+    from paper_2505_10584_b200 import denoise_windows, plan_temporal_windows
+    cfg, grid = CASES[name]
+    clip_grid = (window, grid[1], grid[2])
+    plan = plan_temporal_windows(n_prime, window, stride)
+    W = init_weights(cfg, seed=0)
+    g = torch.Generator().manual_seed(1)
+    pt, ph, pw = cfg.patch
+    x0 = torch.randn(cfg.latent_channels, n_prime * pt, grid[1] * ph, grid[2] * pw, generator=g)
+    inp = synthetic_inputs(cfg, clip_grid)
+    pooled = inp["pooled"] if cfg.family == "mm-dit" else None
+    model = build_model(cfg, weights=W).prepare(clip_grid, inp["text"], pooled)
+    steps = 6
+    sched = plan_cache(steps, warmup=1, interval=2)
+    res = denoise_windows(model, x0, steps, plan, sched, trajectory=True)
+    nf = front_block_count(cfg.num_layers, 0.25)
+    orcs = [ref.OracleDiT(cfg, W, inp["text"], pooled, clip_grid, n_front=nf) for _ in plan.clips]
+    lat = ref.denoise_windows(orcs, x0, steps, plan.clips, flags=sched.per_step_full)
+    errs = [rel_l2(a, b) for a, b in zip(res.trajectory, lat[1:])]
+    assert max(errs) <= TOL_BF16, errs

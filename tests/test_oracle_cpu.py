@@ -128,3 +128,35 @@ def test_config_validation():
         DiTConfig("single-dit", hidden_size=128, num_heads=4, num_dual=1)
     with pytest.raises(ConfigError):
         DiTConfig("mm-dit", hidden_size=128, num_heads=4, num_dual=0, num_single=0)
+
+
+def test_oracle_windows_single_clip_equals_plain_denoise():
+    """Eq. 3 with one clip covering the latent is the plain Euler loop (oracle self-check)."""
+    from oracle import dit_oracle as ref
+    from paper_2505_10584_b200 import TINY_SINGLE
+    from paper_2505_10584_b200.weights import init_weights, synthetic_inputs
+
+    cfg, grid = TINY_SINGLE, (2, 4, 4)
+    W = init_weights(cfg, seed=0)
+    inp = synthetic_inputs(cfg, grid)
+    a = ref.denoise_windows([ref.OracleDiT(cfg, W, inp["text"], None, grid)], inp["x0"], 3, [(0, 2)])
+    b, _, _ = ref.denoise(ref.OracleDiT(cfg, W, inp["text"], None, grid), inp["x0"], 3, flags=[True] * 3)
+    for x, y in zip(a, b):
+        assert torch.allclose(x, y, atol=1e-6)
+
+
+def test_oracle_attention_cache_all_full_equals_no_cache():
+    from oracle import dit_oracle as ref
+    from paper_2505_10584_b200 import TINY_MM
+    from paper_2505_10584_b200.weights import init_weights, synthetic_inputs
+
+    cfg, grid = TINY_MM, (2, 4, 4)
+    W = init_weights(cfg, seed=0)
+    inp = synthetic_inputs(cfg, grid)
+    o1 = ref.OracleDiT(cfg, W, inp["text"], inp["pooled"], grid, mode="attention-cache")
+    o2 = ref.OracleDiT(cfg, W, inp["text"], inp["pooled"], grid)
+    a, _, _ = ref.denoise(o1, inp["x0"], 3, flags=[True] * 3)
+    b, _, _ = ref.denoise(o2, inp["x0"], 3, flags=[True] * 3)
+    assert all(torch.equal(x, y) for x, y in zip(a, b))
+    c, _, _ = ref.denoise(o1, inp["x0"], 3, flags=[True, False, True])
+    assert not torch.equal(c[2], a[2])  # the cached step really reuses stale attention
