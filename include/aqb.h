@@ -37,6 +37,9 @@ extern "C" {
 #define AQB_EUNSUPPORTED (-3)
 
 int aqb_abi_version(void);
+/* sha256 (hex) of this header as compiled into the library — the Python binding
+ * refuses a libaqb.so built from a different header (stale build). */
+const char* aqb_build_id(void);
 const char* aqb_last_error(void);
 int aqb_sm_count(void);
 

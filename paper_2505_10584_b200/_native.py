@@ -20,6 +20,7 @@ c_char_p = ctypes.c_char_p
 P = c_void_p  # every pointer is passed as an integer address
 SIGNATURES = {
     "aqb_abi_version": (c_int, []),
+    "aqb_build_id": (c_char_p, []),
     "aqb_last_error": (c_char_p, []),
     "aqb_sm_count": (c_int, []),
     "aqb_norm_modulate": (c_int, [P, c_int64, P, P, P, c_int64, c_int64, c_int32, c_float, c_int32, P, P, P, c_int32, P]),
@@ -98,6 +99,12 @@ def load():
         fn = getattr(lib, name)
         fn.restype = res
         fn.argtypes = args
+    from .build import header_hash
+
+    built = lib.aqb_build_id().decode()
+    if built != header_hash():
+        raise NativeError(f"{LIB_PATH} was built from a different include/aqb.h ({built[:12]} vs "
+                          f"{header_hash()[:12]}) — rebuild with `python -m paper_2505_10584_b200.build --force`")
     _lib = lib
     return lib
 

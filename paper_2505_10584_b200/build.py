@@ -43,11 +43,20 @@ def _stale() -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
+def header_hash() -> str:
+    """sha256 of include/aqb.h — compiled in as aqb_build_id() and checked at load time."""
+    import hashlib
+
+    with open(os.path.join(INCLUDE, "aqb.h"), "rb") as fh:
+        return hashlib.sha256(fh.read()).hexdigest()
+
+
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
     tmp = LIB + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", INCLUDE, *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
+    cmd = [nvcc(), *NVCC_FLAGS, f'-DAQB_HEADER_HASH="{header_hash()}"', "-I", INCLUDE,
+           *[os.path.join(CSRC, s) for s in SOURCES], "-o", tmp]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)

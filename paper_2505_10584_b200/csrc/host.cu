@@ -79,6 +79,11 @@ extern "C" {
 
 int aqb_abi_version(void) { return AQB_ABI_VERSION; }
 
+#ifndef AQB_HEADER_HASH
+#define AQB_HEADER_HASH "unknown"
+#endif
+const char* aqb_build_id(void) { return AQB_HEADER_HASH; }
+
 const char* aqb_last_error(void) { return aqb::last_error(); }
 
 int aqb_sm_count(void) { return aqb::sm_count(); }

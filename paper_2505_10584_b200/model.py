@@ -37,7 +37,7 @@ import torch
 from . import ops
 from .config import DiTConfig
 from .errors import ConfigError
-from .parallel import SIGNAL_BYTES, PeerBuffers, Ulysses
+from .parallel import SIGNAL_BYTES, PeerBuffers, Ulysses, exchange_offsets
 from .schedule import front_block_count
 from .weights import init_weights
 
@@ -196,9 +196,9 @@ class DiTModel:
                                                   "sig": SIGNAL_BYTES}, dev)
                 self.a2a_rcv = self.peer.local("rcv", (Sv + St, 3, hl, D), BF16)
                 self.o = self.peer.local("o", (rows, H), BF16)
-                r = self.sp.rank
-                self.qkv_dst = self.peer.ptrs("rcv", r * Sv_loc * rs * 2)
-                self.o_dst = self.peer.ptrs("o", r * hl * D * 2)
+                off = exchange_offsets(self.sp.rank, P, Sv_loc, hl, D, H)
+                self.qkv_dst = self.peer.ptrs("rcv", off["qkv"])
+                self.o_dst = self.peer.ptrs("o", off["o"])
                 self.sig = self.peer.ptrs("sig")
                 self.epoch = torch.zeros(1, device=dev, dtype=torch.int32)
                 self.peer_status = torch.zeros(1, device=dev, dtype=torch.int32)
@@ -358,9 +358,13 @@ class DiTModel:
         xo = self._xo
         if not askip:
             ops.norm_modulate(self.x, None, None, self.m, eps, kind=2, run_flag=aflag, run_if=arun)
-            ops.gemm(self.m, W[f"{p}.xq.w"], self.xq, bias=W[f"{p}.xq.b"], run_flag=aflag, run_if=arun)
-            ops.qk_norm_rope(self.xq, A, D, W[f"{p}.xq_norm"], None, cfg.qk_norm_eps, parts=1, norm_parts=1,
-                             run_flag=aflag, run_if=arun)
+            if D == 128 and not self.fp32:  # q projection with the QK-RMSNorm fused in its epilogue
+                ops.gemm_qknorm_rope(self.m, W[f"{p}.xq.w"], self.xq, H, 1, W[f"{p}.xq_norm"], None,
+                                     cfg.qk_norm_eps, bias=W[f"{p}.xq.b"], run_flag=aflag, run_if=arun)
+            else:
+                ops.gemm(self.m, W[f"{p}.xq.w"], self.xq, bias=W[f"{p}.xq.b"], run_flag=aflag, run_if=arun)
+                ops.qk_norm_rope(self.xq, A, D, W[f"{p}.xq_norm"], None, cfg.qk_norm_eps, parts=1, norm_parts=1,
+                                 run_flag=aflag, run_if=arun)
             kv = self.text_kv[i]
             ops.attention(self.xq, kv, kv[:, H:], xo, A, D, workspace=self.attn_ws, run_flag=aflag, run_if=arun)
         ops.gemm(xo, W[f"{p}.xproj.w"], self.x, bias=W[f"{p}.xproj.b"], epilogue="gate_res", run_flag=flag,

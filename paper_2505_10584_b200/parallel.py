@@ -85,6 +85,23 @@ def init_from_env(backend: str | None = None):
     dist.init_process_group(backend=backend)
 
 
+def exchange_offsets(rank: int, P: int, rows_per_rank: int, heads_per_rank: int, head_dim: int, hidden: int,
+                     elem_bytes: int = 2) -> dict:
+    """Byte offsets this rank adds to every peer's base pointer for the fused exchange.
+
+    * ``qkv``: into each peer's attention input ``[S_v + S_t, 3, A/P, D]`` — this rank's
+      video rows start at row ``rank * S_v/P`` (row stride ``3·(A/P)·D``);
+    * ``o``: into each peer's attention output ``[S_v/P + S_t, H]`` — this rank's heads
+      are columns ``[rank·(A/P)·D, (rank+1)·(A/P)·D)``.
+    """
+    if not 0 <= rank < P:
+        raise ConfigError(f"rank {rank} outside [0, {P})", "parallel.rank")
+    row = 3 * heads_per_rank * head_dim
+    if heads_per_rank * head_dim * P != hidden:
+        raise ConfigError("hidden != P * heads_per_rank * head_dim", "parallel.ulysses")
+    return {"qkv": rank * rows_per_rank * row * elem_bytes, "o": rank * heads_per_rank * head_dim * elem_bytes}
+
+
 class _DeviceBytes:
     """``__cuda_array_interface__`` view of a libaqb allocation (so torch can wrap it)."""
 
@@ -147,7 +164,8 @@ class PeerBuffers:
     def close(self):
         """Unmap peers and free this rank's buffers (collective: barrier first)."""
         dist.barrier(group=self.sp.group)
-        torch.cuda.synchronize()
+        if self.device.type == "cuda":
+            torch.cuda.synchronize(self.device)
         for p in self._opened:
             _native.call("aqb_peer_close", p)
         for p in self._own.values():
