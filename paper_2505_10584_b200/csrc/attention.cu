@@ -366,8 +366,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       // TMA coordinates must be >= 0: a tile that starts in one rank's rows and ends in
       // the next (or in the text rows) is written with direct stores instead.
       const int64_t last = min(int64_t(tr0 + BQ - 1), int64_t(p.seq_q - 1));
-      const bool use_tma = m.nranks == 0 || tr0 >= m.text_row0 ||
-                           (last < m.text_row0 && tr0 / m.rows_per_rank == last / m.rows_per_rank);
+      const bool use_tma = tr0 < p.seq_q &&  // a tile wholly past the end stores nothing
+                           (m.nranks == 0 || tr0 >= m.text_row0 ||
+                            (last < m.text_row0 && tr0 / m.rows_per_rank == last / m.rows_per_rank));
 #pragma unroll 1
       for (int cc = 0; cc < D / 32; ++cc) {
         uint32_t u[32];

@@ -8,6 +8,8 @@ fallback path: a missing library or a non-CUDA tensor raises.
 
 from __future__ import annotations
 
+import os
+
 import torch
 
 from . import _native
@@ -55,8 +57,18 @@ def set_profiler(p: KernelProfiler | None):
     _PROF = p
 
 
+_SYNC_DEBUG = bool(os.environ.get("AQB_SYNC_DEBUG"))
+
+
 def _run(kind, work, name, *args):
     prof = _PROF
+    if _SYNC_DEBUG:  # debugging aid: fail at the launch that faults, naming it
+        _native.call(name, *args)
+        try:
+            torch.cuda.synchronize()
+        except Exception as e:
+            raise NativeError(f"{name} faulted: {e}") from e
+        return
     if prof is None:
         _native.call(name, *args)
         return

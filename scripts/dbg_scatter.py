@@ -3,8 +3,9 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 from paper_2505_10584_b200 import ops
 dev = "cuda"
 case = sys.argv[1]
-P, hl, d = 4, 2, 128
-rpr, St = {"aligned": (256, 0), "text": (256, 128), "straddle": (300, 0), "straddle_text": (300, 40)}[case]
+P, hl, d = (2, 4, 128) if case == "odd_tiles" else (4, 2, 128)
+rpr, St = {"aligned": (256, 0), "text": (256, 128), "straddle": (300, 0), "straddle_text": (300, 40),
+           "odd_tiles": (192, 0)}[case]
 H = P * hl * d
 sq = P * rpr + St
 qkv = torch.randn(sq, 3, hl, d, device=dev).to(torch.bfloat16)

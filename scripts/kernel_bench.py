@@ -124,6 +124,8 @@ def main():
         res.append(attn_case(S, 256, 16, 128, args.ncu))
         if not args.ncu:
             res.append(attn_case(118800 + 256, 118800 + 256, 3, 128))  # config 4 per rank at P=8
+    if args.only == "attn-long":  # config 4 per rank at P=8 (and the 1-GPU per-head shape)
+        res.append(attn_case(118800 + 256, 118800 + 256, 3, 128, args.ncu))
     if args.only in ("all", "norm"):
         res.append(norm_case(S, H, args.ncu))
         res.append(qk_case(S, 16, 128, args.ncu))

@@ -27,6 +27,9 @@ KEYS = [
     ("launch__grid_size", "grid"),
     ("launch__block_size", "block"),
     ("smsp__warps_issue_stalled_long_scoreboard_per_warp_active.pct", "stall_long_sb_%"),
+    ("smsp__issue_active.avg.pct_of_peak_sustained_active", "issue_active_%"),
+    ("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active", "alu_pipe_%"),
+    ("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed", "smem_pipe_%"),
 ]
 
 
