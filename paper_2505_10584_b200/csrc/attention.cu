@@ -25,6 +25,7 @@
 // TMEM: S0 | S1 | O0 | O1  (128 + 128 + D + D columns).
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 
 #include "host.cuh"
@@ -38,7 +39,7 @@ constexpr int BKV = 128;  // keys per KV tile (MMA N of QK^T, K of PV)
 constexpr int kThreads = 384;    // 3 warpgroups: control | softmax tile 0 | softmax tile 1
 constexpr uint32_t kCtrlRegs = 56;     // setmaxnreg budgets: 56 + 2 * 224 <= 512 per SMSP
 constexpr uint32_t kSoftmaxRegs = 224;
-constexpr uint32_t kPolyMask = 0x52;
+constexpr uint32_t kPolyMaskDefault = 0x52;
 constexpr uint32_t kPCol = 64;         // P_t (bf16 pairs) lives in columns 64..127 of S_t   // pairs (i & 7) in {1,4,6}: exp2 by polynomial (3/8 off the MUFU)
 
 template <int D>
@@ -107,7 +108,7 @@ __device__ __forceinline__ void for_each_out(const OutMap& m, int head, int64_t 
   }
 }
 
-template <int D>
+template <int D, uint32_t kPolyMask = kPolyMaskDefault>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ OutMaps om, Params p) {
@@ -262,10 +263,18 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < BKV; ++i)
           if (i >= kv_valid) sr[i] = 0xff800000u;  // -inf
       }
-      float mx = __uint_as_float(sr[0]);
+      // row max as 8 independent FMNMX3 chains + a 3-level tree (a single 64-long
+      // dependent chain was the softmax's critical path)
+      float mm[8];
 #pragma unroll
-      for (int i = 1; i + 1 < BKV; i += 2) mx = fmaxf(mx, fmaxf(__uint_as_float(sr[i]), __uint_as_float(sr[i + 1])));
-      mx = fmaxf(mx, __uint_as_float(sr[BKV - 1]));
+      for (int k = 0; k < 8; ++k) mm[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
+#pragma unroll
+      for (int i = 16; i < BKV; i += 16)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          mm[k] = fmaxf(mm[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
+      const float mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
+                             fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
       // PV_{j-1} must be done before O is rescaled or P_t overwritten.
       if (j > 0) {
         mbar_wait(o_ready + t, (j - 1) & 1);
@@ -293,7 +302,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const float nm = -m_run * c;
       const uint64_t nm2 = f2pack(nm, nm);
-      uint64_t acc2 = f2pack(0.f, 0.f);
+      uint64_t acc2[4];  // 4 independent packed row-sum chains
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc2[q] = f2pack(0.f, 0.f);
       uint32_t pp[16];  // 16 packed bf16 pairs = 16 TMEM columns, stored as they fill
 #pragma unroll
       for (int kc = 0; kc < BKV / 8; ++kc) {
@@ -320,13 +331,13 @@ __global__ void __launch_bounds__(kThreads, 1)
             p0 = ex2(x0);
             p1 = ex2(x1);
           }
-          acc2 = fadd2(acc2, f2pack(p0, p1));
+          acc2[q] = fadd2(acc2[q], f2pack(p0, p1));
           pp[(kc & 3) * 4 + q] = pack_bf16(p0, p1);
         }
         if ((kc & 3) == 3) tmem_st16(s_tmem + kPCol + (kc >> 2) * 16, pp);
       }
       float a0, a1;
-      f2unpack(acc2, a0, a1);
+      f2unpack(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])), a0, a1);
       l_run += a0 + a1;
       tmem_wait_st();  // P in TMEM before the MMA warp may read it
       tc_fence_before();
@@ -520,9 +531,17 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     if (rc) return rc;
   }
   constexpr int smem = Cfg<D>::kSmem;
+  // AQB_ATTN_POLY (tuning): which of every 8 exp2 pairs run on the FMA pipe instead of MUFU
+  static int poly = -1;
+  if (poly < 0) {
+    const char* e = getenv("AQB_ATTN_POLY");
+    poly = (e && !strcmp(e, "0")) ? 0 : (e && !strcmp(e, "2")) ? 2 : (e && !strcmp(e, "4")) ? 4 : 3;
+  }
+  auto kern = poly == 0 ? attn_fwd_kernel<D, 0x00> : poly == 2 ? attn_fwd_kernel<D, 0x22>
+                       : poly == 4 ? attn_fwd_kernel<D, 0x55> : attn_fwd_kernel<D, kPolyMaskDefault>;
   static bool configured = false;
   if (!configured) {
-    AQB_CUDA_TRY(cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    AQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     configured = true;
   }
   OutMaps om;
@@ -533,7 +552,7 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     memset(&om, 0, sizeof(om));
   }
   dim3 grid((p.seq_q + 2 * BQ - 1) / (2 * BQ), p.heads, p.splits);
-  attn_fwd_kernel<D><<<grid, kThreads, smem, stream>>>(tq, tk, tv, om, p);
+  kern<<<grid, kThreads, smem, stream>>>(tq, tk, tv, om, p);
   AQB_LAUNCH_CHECK();
   if (p.splits > 1) {
     const int64_t warps = static_cast<int64_t>(p.seq_q) * p.heads;

@@ -3,6 +3,7 @@
 
     python scripts/ncu_summary.py report <file.ncu-rep>   # per-kernel key metrics (--set full capture)
     python scripts/ncu_summary.py launches <file.csv>     # launch-list time shares (gpu__time_duration pass)
+    python scripts/ncu_summary.py sass <file.ncu-rep>     # executed-instruction mix + top stall sites
 """
 
 import collections
@@ -70,5 +71,33 @@ def launches(path):
         print(f"{k:40s} {cnt[k]:6d} {v / 1e6:10.3f} ms {100 * v / T:6.1f}%")
 
 
+
+
+def sass(path, top=20):
+    out = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "sass"],
+                         capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    h = rows[1]
+    ix = {k: i for i, k in enumerate(h)}
+    data = [r for r in rows[2:] if len(r) >= len(h)]
+    ex, st = collections.Counter(), collections.Counter()
+    for r in data:
+        src = r[ix["Source"]].strip().split()
+        op = (src[1] if src and src[0].startswith("@") and len(src) > 1 else (src[0] if src else "")).split(".")[0]
+        ex[op] += int(r[ix["Instructions Executed"]] or 0)
+        st[op] += int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+    tot, tots = sum(ex.values()), sum(st.values())
+    print(f"# executed warp instructions: {tot}; stall samples: {tots}")
+    print("## instruction mix (executed share, stall-sample share)")
+    for op, c in ex.most_common(top):
+        print(f"  {op:10s} {c / tot * 100:5.1f}%  {st[op] / max(tots, 1) * 100:5.1f}%")
+    print("## top stall sites")
+    a0 = int(data[0][0], 16)
+    for r in sorted(data, key=lambda r: -int(r[ix["Warp Stall Sampling (All Samples)"]] or 0))[:top]:
+        n = int(r[ix["Warp Stall Sampling (All Samples)"]] or 0)
+        print(f"  +{int(r[0], 16) - a0:#07x} {n / max(tots, 1) * 100:5.1f}%  exec {r[ix['Instructions Executed']]:>12s}  "
+              f"{r[ix['Source']].strip()[:60]}")
+
+
 if __name__ == "__main__":
-    {"report": report, "launches": launches}[sys.argv[1]](sys.argv[2])
+    {"report": report, "launches": launches, "sass": sass}[sys.argv[1]](sys.argv[2])
