@@ -65,7 +65,9 @@ int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift, const flo
  * epilogue:
  *   AQB_EPI_BF16       out bf16 = acc + bias
  *   AQB_EPI_GELU_BF16  out bf16 = gelu_tanh(acc + bias)
- *   AQB_EPI_GATE_RES   out f32 (in/out residual) += gate[n] * (acc + bias)
+ *   AQB_EPI_GATE_RES   out f32 (in/out residual) += gate[n] * (acc + bias); if aux != NULL
+ *                      also aux bf16 (stride ld_aux) = bf16(new out) — the next projection's A
+ *                      operand, so no separate cast pass
  *   AQB_EPI_F32        out f32 = acc + bias
  *   AQB_EPI_EULER      out f32 (latent, in/out) += (*alpha) * (acc + bias);
  *                      aux bf16 (stride ld_aux) = bf16(new out)   [flow-matching Euler step]

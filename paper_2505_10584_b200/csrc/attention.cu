@@ -190,11 +190,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           umma_bf16_ss(tmem + t * 128, smem_desc(a0 + off, 0, 1024), smem_desc(b0 + off, 0, 1024), kIdescS, kk > 0);
         }
       };
-      auto issue_pv = [&](int t, int stage, bool acc) {
+      auto issue_pv = [&](int t, int stage, bool acc, int kk0, int kk1) {
         // A = P_t straight from TMEM (columns 64..127 of S_t, bf16 pairs), B = V (MN-major smem)
         const uint32_t a0 = tmem + t * 128 + kPCol, b0 = kv_addr + stage * C::kKVBytes;
 #pragma unroll
-        for (int kk = 0; kk < BKV / 16; ++kk) {
+        for (int kk = kk0; kk < kk1; ++kk) {
           const uint32_t boff = kk * 16 * 128;  // 16 keys x 128 B rows
           umma_bf16_ts(tmem + 256 + t * D, a0 + kk * 8, smem_desc(b0 + boff, BKV * 128, 1024), kIdescO,
                        (acc || kk > 0) ? 1u : 0u);
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(kv_full + iv % C::NS, (iv / C::NS) & 1);
           mbar_wait(p_full + 0, (j - 1) & 1);
           tc_fence_after();
-          issue_pv(0, iv % C::NS, j > 1);
+          issue_pv(0, iv % C::NS, j > 1, 0, BKV / 16);
           umma_commit(o_ready + 0);
         }
         if (j < nkv) {
@@ -222,7 +222,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j > 0) {
           mbar_wait(p_full + 1, (j - 1) & 1);
           tc_fence_after();
-          issue_pv(1, iv % C::NS, j > 1);
+          issue_pv(1, iv % C::NS, j > 1, 0, BKV / 16);
           umma_commit(o_ready + 1);
           umma_commit(kv_empty + iv % C::NS);
         }

@@ -107,6 +107,88 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
   }
 }
 
+// CTA per row for wide rows (hidden >= 1024): hidden/16 threads, 4 float4 each,
+// so a few thousand rows (one Ulysses shard) still fill the SMs with enough
+// loads in flight; block reductions through shared memory.
+template <int NW>
+AQB_DEV float block_sum(float v, float* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();  // red[] reuse across calls
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  float t = 0.f;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) t += red[i];
+  return t;
+}
+
+template <int NW, typename OutT>
+__global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __restrict__ x, int64_t ldx,
+                                                               const float* __restrict__ shift,
+                                                               const float* __restrict__ scale, OutT* __restrict__ y,
+                                                               int64_t ldy, int64_t rows, float eps, int kind,
+                                                               float* __restrict__ prev, float* __restrict__ partials,
+                                                               const int32_t* flag, int32_t run_if) {
+  if (!gate_open(flag, run_if)) return;
+  __shared__ float red[NW];
+  constexpr int T = NW * 32, H = T * 16;
+  const int64_t row = blockIdx.x;
+  const int tid = threadIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
+  float4 v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = ld_stream(xr + tid + T * j);
+  float mean = 0.f;
+  if (kind == 0) {
+    float s = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    mean = block_sum<NW>(s, red) * (1.f / H);
+  }
+  float rstd = 1.f;
+  if (kind != 2) {
+    float ss = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
+      ss += (a * a + b * b) + (c * c + d * d);
+    }
+    rstd = rsqrtf(block_sum<NW>(ss, red) * (1.f / H) + eps);
+  }
+  const float4* sh4 = reinterpret_cast<const float4*>(shift);
+  const float4* sc4 = reinterpret_cast<const float4*>(scale);
+  OutT* yr = y + row * ldy;
+  float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
+  float dsum = 0.f, psum = 0.f;
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c4 = tid + T * j;
+    const float4 sc = scale ? __ldg(sc4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4 sh = shift ? __ldg(sh4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    float4 o;
+    o.x = (v[j].x - mean) * rstd * (1.f + sc.x) + sh.x;
+    o.y = (v[j].y - mean) * rstd * (1.f + sc.y) + sh.y;
+    o.z = (v[j].z - mean) * rstd * (1.f + sc.z) + sh.z;
+    o.w = (v[j].w - mean) * rstd * (1.f + sc.w) + sh.w;
+    store4(yr + 4 * c4, o);
+    if (pr) {
+      const float4 p = pr[c4];
+      dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
+      psum += (fabsf(p.x) + fabsf(p.y)) + (fabsf(p.z) + fabsf(p.w));
+      pr[c4] = o;
+    }
+  }
+  if (pr) {
+    dsum = block_sum<NW>(dsum, red);
+    psum = block_sum<NW>(psum, red);
+    if (tid == 0) {
+      partials[row] = dsum;
+      partials[rows + row] = psum;
+    }
+  }
+}
+
 // ------------------------------------------------------- QK-norm + 3D RoPE
 // One warp per (row, head); lane handles pairs lane, lane+32, ... (D/2 pairs).
 template <int D, typename T>
@@ -371,6 +453,20 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
   const int grid = static_cast<int>((rows + 7) / 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
   OutT* yb = reinterpret_cast<OutT*>(y);
+  if (hidden >= 1024 && hidden % 512 == 0) {  // CTA per row (hidden/16 threads)
+    switch (hidden / 512) {
+#define NMR_CASE(NW)                                                                                               \
+  case NW:                                                                                                         \
+    norm_mod_row_kernel<NW, OutT><<<unsigned(rows), NW * 32, 0, s>>>(x, ldx, shift, scale, yb, ldy, rows, eps,     \
+                                                                     norm_kind, probe_prev, probe_partials,        \
+                                                                     run_flag, run_if);                            \
+    AQB_LAUNCH_CHECK();                                                                                            \
+    return AQB_OK;
+      NMR_CASE(2) NMR_CASE(3) NMR_CASE(4) NMR_CASE(5) NMR_CASE(6) NMR_CASE(7) NMR_CASE(8)
+#undef NMR_CASE
+      default: break;
+    }
+  }
 #define NM_CASE(NV)                                                                                          \
   case NV:                                                                                                   \
     norm_mod_kernel<NV, OutT><<<grid, 256, 0, s>>>(x, ldx, shift, scale, yb, ldy, rows, eps, norm_kind,      \

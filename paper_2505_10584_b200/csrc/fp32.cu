@@ -68,7 +68,12 @@ __global__ void __launch_bounds__(256) gemm_kernel(const float* __restrict__ A, 
       float* o = out + static_cast<int64_t>(m) * ldo + n;
       switch (epi) {
         case AQB_EPI_GELU_BF16: *o = gelu_precise(v); break;
-        case AQB_EPI_GATE_RES: *o += (gate ? gate[n] : 1.f) * v; break;
+        case AQB_EPI_GATE_RES: {
+          const float x = *o + (gate ? gate[n] : 1.f) * v;
+          *o = x;
+          if (aux) aux[static_cast<int64_t>(m) * ld_aux + n] = x;
+          break;
+        }
         case AQB_EPI_EULER: {
           const float x = *o + al * v;
           *o = x;

@@ -40,6 +40,7 @@ constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
 constexpr int kThreads = 256;
 constexpr int kEpiBuf = 128 * 128;  // one epilogue chunk: 128 rows x 128 B
+constexpr int kAuxBuf = 128 * 64;   // bf16 copy of a gate*residual chunk: 128 rows x 64 B (64B swizzle)
 
 struct Params {
   int M, N, K;
@@ -126,7 +127,7 @@ __device__ __forceinline__ void euler_chunk(const Params& p, int row, int col0, 
 
 // Per-CTA epilogue state (warps 4-7 only).
 struct EpiState {
-  uint8_t* buf;      // kEpiBufs(EPI) x kEpiBuf, 1024-aligned
+  uint8_t* buf;      // kEpiBufs(EPI) x kEpiBuf, 1024-aligned (gate*residual: + 2 x kAuxBuf bf16 copies)
   uint64_t* bar;     // one mbarrier per buffer (residual TMA loads)
   uint32_t chunk;    // chunks processed by this CTA (buffer / phase bookkeeping)
 };
@@ -135,6 +136,9 @@ struct EpiState {
 // while chunk c is combined; the store-only epilogues need two.
 template <int EPI>
 constexpr int epi_bufs() { return EPI == AQB_EPI_GATE_RES ? 3 : 2; }
+
+template <int EPI>
+constexpr int aux_bytes() { return EPI == AQB_EPI_GATE_RES ? 2 * kAuxBuf : 0; }
 
 template <int EPI>
 constexpr int epi_cols() { return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES) ? 32 : 64; }
@@ -302,18 +306,34 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       }
       const uint32_t rowaddr = smem_u32(buf) + r * 128;
       const uint32_t sw = r & 7;
+      uint8_t* abuf = es.buf + NB * kEpiBuf + (es.chunk & 1) * kAuxBuf;
       if constexpr (EPI == AQB_EPI_GATE_RES) {
+        if (p.aux != nullptr) {  // the aux buffer was last stored two chunks ago
+          if (leader_thread) bulk_wait_read<1>();
+          named_bar_sync(1, 128);
+        }
         mbar_wait(es.bar + b, (es.chunk / NB) & 1);
         const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
+        const uint32_t arow = smem_u32(abuf) + r * 64, asw = (r >> 1) & 3;
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          const uint32_t a = rowaddr + ((i ^ sw) << 4);
-          const uint4 xr = lds128(a);
-          const float4 g = (p.gate && col0 + 4 * i < p.N) ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
-          st_shared_v4(a, __float_as_uint(__uint_as_float(xr.x) + g.x * v[4 * i]),
-                       __float_as_uint(__uint_as_float(xr.y) + g.y * v[4 * i + 1]),
-                       __float_as_uint(__uint_as_float(xr.z) + g.z * v[4 * i + 2]),
-                       __float_as_uint(__uint_as_float(xr.w) + g.w * v[4 * i + 3]));
+        for (int i = 0; i < 8; i += 2) {
+          float nx[8];
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const uint32_t a = rowaddr + (((i + h) ^ sw) << 4);
+            const uint4 xr = lds128(a);
+            const float4 g = (p.gate && col0 + 4 * (i + h) < p.N) ? __ldg(g4 + i + h)
+                                                                    : make_float4(1.f, 1.f, 1.f, 1.f);
+            nx[4 * h + 0] = __uint_as_float(xr.x) + g.x * v[4 * (i + h)];
+            nx[4 * h + 1] = __uint_as_float(xr.y) + g.y * v[4 * (i + h) + 1];
+            nx[4 * h + 2] = __uint_as_float(xr.z) + g.z * v[4 * (i + h) + 2];
+            nx[4 * h + 3] = __uint_as_float(xr.w) + g.w * v[4 * (i + h) + 3];
+            st_shared_v4(a, __float_as_uint(nx[4 * h]), __float_as_uint(nx[4 * h + 1]),
+                         __float_as_uint(nx[4 * h + 2]), __float_as_uint(nx[4 * h + 3]));
+          }
+          if (p.aux != nullptr)  // bf16(new residual): the next projection's A operand
+            st_shared_v4(arow + (((i >> 1) ^ asw) << 4), pack_bf16(nx[0], nx[1]), pack_bf16(nx[2], nx[3]),
+                         pack_bf16(nx[4], nx[5]), pack_bf16(nx[6], nx[7]));
         }
       } else if constexpr (EPI == AQB_EPI_F32) {
 #pragma unroll
@@ -334,6 +354,9 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       named_bar_sync(1, 128);
       if (leader_thread) {
         tma_store_2d(tmo, buf, col0, row0);  // clips rows >= M and columns >= N
+        if constexpr (EPI == AQB_EPI_GATE_RES) {
+          if (p.aux != nullptr) tma_store_2d(&pm->m[0], abuf, col0, row0);
+        }
         bulk_commit();
       }
       ++es.chunk;
@@ -343,7 +366,8 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 
 template <int BN, int STAGES, bool PAIR, int EPI>
 constexpr int smem_bytes() {
-  return STAGES * (BM + (PAIR ? BN / 2 : BN)) * BK * 2 + epi_bufs<EPI>() * kEpiBuf + 1024 /*align*/ + 256 /*bars*/;
+  return STAGES * (BM + (PAIR ? BN / 2 : BN)) * BK * 2 + epi_bufs<EPI>() * kEpiBuf + aux_bytes<EPI>() +
+         1024 /*align*/ + 256 /*bars*/;
 }
 
 template <int BN, int STAGES, int EPI>
@@ -356,7 +380,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(base);
   __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(base + STAGES * BM * BK * 2);
   uint8_t* ebuf = base + STAGES * (BM + BN) * BK * 2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf + aux_bytes<EPI>());
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -472,7 +496,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sa = base;
   uint8_t* sb = base + STAGES * kABytes;
   uint8_t* ebuf = base + STAGES * (kABytes + kBBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf + aux_bytes<EPI>());
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
@@ -614,7 +638,10 @@ template <int BN, int STAGES, bool PAIR>
 int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const PeerMaps& pm,
                  const Params& p, cudaStream_t s) {
   // one pipeline stage makes room for the third gate*residual buffer
-  constexpr int kResStages = STAGES - ((PAIR ? BM + BN / 2 : BM + BN) * BK * 2 >= kEpiBuf * 2 ? 1 : 1);
+  // gate*residual: 3 f32 buffers + 2 bf16 aux buffers; drop pipeline stages until it fits
+  constexpr int kStageBytes = (PAIR ? BM + BN / 2 : BM + BN) * BK * 2;
+  constexpr int kFixed = 3 * kEpiBuf + 2 * kAuxBuf + 1024 + 256;
+  constexpr int kResStages = (232448 - kFixed) / kStageBytes < STAGES ? (232448 - kFixed) / kStageBytes : STAGES;
   switch (epi) {
     case AQB_EPI_BF16: return launch<BN, STAGES, AQB_EPI_BF16, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16, PAIR>(ta, tb, to, pm, p, s);
@@ -742,6 +769,19 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
   p.out = out, p.ldo = ldo, p.bias = bias, p.gate = gate, p.alpha = alpha;
   p.aux = reinterpret_cast<__nv_bfloat16*>(aux), p.ld_aux = ld_aux;
   p.run_flag = run_flag, p.run_if = run_if;
+  if (epilogue == AQB_EPI_GATE_RES && aux != nullptr) {
+    // bf16 copy of the new residual, TMA-stored beside it (64B-swizzled 32-column chunks)
+    AQB_CHECK_ARG(ld_aux >= n && ld_aux % 8 == 0, "gemm: bad ld_aux");
+    PeerMaps xm;
+    memset(&xm, 0, sizeof(xm));
+    const uint64_t dims[2] = {uint64_t(n), uint64_t(m)};
+    const uint64_t strides[1] = {uint64_t(ld_aux) * 2};
+    const uint32_t box[2] = {32, uint32_t(BM)};
+    int rc = make_tmap(&xm.m[0], CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, aux, 2, dims, strides, box,
+                       CU_TENSOR_MAP_SWIZZLE_64B);
+    if (rc) return rc;
+    return run(a, lda, w, ldw, m, n, k, epilogue, p, to, variant, reinterpret_cast<cudaStream_t>(stream), &xm);
+  }
   return run(a, lda, w, ldw, m, n, k, epilogue, p, to, variant, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -53,6 +53,24 @@ AQB_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
   while (!mbar_try_wait(a, parity)) {
   }
 }
+// try_wait with a suspend-time hint: the waiting warp is parked by the barrier
+// unit until the phase completes (or the hint expires) instead of re-issuing
+// try_wait/branch — spinning warps steal issue slots from working warps on the
+// same SM sub-partition.
+AQB_DEV bool mbar_try_wait_sleep(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n selp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity), "r"(0x989680u)
+      : "memory");
+  return ok != 0;
+}
+AQB_DEV void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_try_wait_sleep(a, parity)) {
+  }
+}
 
 // ---------------------------------------------------------------------- TMA
 // L2 cache-policy operands (createpolicy.fractional encodings).

@@ -352,12 +352,13 @@ class DiTModel:
             self._decide()
         if not askip:
             self._qkv_attention(p, None, aflag, arun)
+        # the out-projection also writes bf16(x): the cross-attention q projection's input
+        # (no norm before cross-attention, PixArt-α) without a separate cast pass
         ops.gemm(self._ob, W[f"{p}.proj.w"], self.x, bias=W[f"{p}.proj.b"], gate=mods[2], epilogue="gate_res",
-                 run_flag=flag, run_if=run_if)
-        # cross-attention to the text (no norm before it, PixArt-α); K/V precomputed per call
+                 aux=self.m, run_flag=flag, run_if=run_if)
+        # cross-attention to the text; K/V precomputed per call
         xo = self._xo
         if not askip:
-            ops.norm_modulate(self.x, None, None, self.m, eps, kind=2, run_flag=aflag, run_if=arun)
             if D == 128 and not self.fp32:  # q projection with the QK-RMSNorm fused in its epilogue
                 ops.gemm_qknorm_rope(self.m, W[f"{p}.xq.w"], self.xq, H, 1, W[f"{p}.xq_norm"], None,
                                      cfg.qk_norm_eps, bias=W[f"{p}.xq.b"], run_flag=aflag, run_if=arun)

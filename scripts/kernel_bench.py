@@ -112,11 +112,14 @@ def main():
     args = ap.parse_args()
     res = []
     S, H = 7800, 2048
-    if args.only in ("all", "gemm", "gemm-proj"):
+    if args.only in ("all", "gemm", "gemm-proj", "gemm-small"):
         shapes = [(S, 3 * H, H, "bf16"), (S, H, H, "gate_res"), (S, 4 * H, H, "gelu"), (S, H, 4 * H, "gate_res"),
                   (14850 + 256, 3 * 3072, 3072, "bf16"), (8192, 8192, 8192, "bf16")]
         if args.only == "gemm-proj":
             shapes = [(S, H, H, "bf16"), (S, H, H, "f32"), (S, H, H, "gate_res")]
+        if args.only == "gemm-small":  # one rank's shard at 4 / 8 GPUs (config 2)
+            shapes = [(m, n, k, e) for m in (S // 4, S // 8)
+                      for (n, k, e) in ((3 * H, H, "bf16"), (H, H, "gate_res"), (4 * H, H, "gelu"), (H, 4 * H, "gate_res"))]
         for (m, n, k, e) in shapes:
             res.append(gemm_case(m, n, k, e, args.ncu))
     if args.only in ("all", "attn"):
@@ -128,6 +131,10 @@ def main():
         res.append(attn_case(118800 + 256, 118800 + 256, 3, 128, args.ncu))
     if args.only in ("all", "norm"):
         res.append(norm_case(S, H, args.ncu))
+        if not args.ncu:
+            res.append(norm_case(S // 4, H))   # one rank's shard at 4 GPUs
+            res.append(norm_case(S // 8, H))   # ... at 8 GPUs
+            res.append(norm_case(14850 + 256, 3072))
         res.append(qk_case(S, 16, 128, args.ncu))
     if args.attn_sweep:
         for s in (4096, 8192, 16384, 32768, 65536, 131072):

@@ -67,6 +67,22 @@ def test_gemm_epilogues(epi):
         assert rel_l2(aux, exp) < 8e-3
 
 
+@pytest.mark.parametrize("m,n,k", [(777, 512, 384), (7800, 2048, 2048), (975, 2048, 8192), (300, 96, 64)])
+def test_gemm_gate_res_with_bf16_copy(m, n, k):
+    """gate*residual epilogue that also TMA-stores bf16(new residual) (the next projection's A)."""
+    g = torch.Generator(device=dev).manual_seed(m + n)
+    a = torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16)
+    w = (torch.randn(n, k, device=dev, generator=g) * 0.05).to(torch.bfloat16)
+    bias = torch.randn(n, device=dev, generator=g)
+    gate = torch.randn(n, device=dev, generator=g)
+    res = torch.randn(m, n, device=dev, generator=g)
+    exp = res + gate * (a.float() @ w.float().t() + bias)
+    aux = torch.full((m, n + 8), 7.0, device=dev, dtype=torch.bfloat16)[:, :n]
+    ops.gemm(a, w, res, bias=bias, gate=gate, epilogue="gate_res", aux=aux)
+    assert rel_l2(res, exp) < 1e-5
+    assert torch.equal(aux, res.to(torch.bfloat16))  # exactly the rounded new residual
+
+
 def test_gemm_run_flag_skips():
     a = torch.ones(128, 64, device=dev, dtype=torch.bfloat16)
     w = torch.ones(64, 64, device=dev, dtype=torch.bfloat16)
@@ -114,7 +130,7 @@ def test_attention_large_logits_rescale():
     assert rel_l2(o, _attn_ref(q, k, v)) < 1e-2
 
 
-@pytest.mark.parametrize("hidden,kind", [(128, 0), (2048, 0), (3072, 0), (2048, 1)])
+@pytest.mark.parametrize("hidden,kind", [(128, 0), (2048, 0), (3072, 0), (2048, 1), (4096, 0), (1024, 2), (3072, 1)])
 def test_norm_modulate(hidden, kind):
     rows = 1000
     g = torch.Generator(device=dev).manual_seed(hidden)
@@ -125,13 +141,16 @@ def test_norm_modulate(hidden, kind):
     ops.norm_modulate(x, shift, scale, out, eps=1e-6, kind=kind)
     if kind == 0:
         exp = ref.modulate(x.cpu(), shift.cpu(), scale.cpu(), 1e-6)
+    elif kind == 2:
+        exp = x.cpu() * (1 + scale.cpu()) + shift.cpu()
     else:
         exp = x.cpu() * torch.rsqrt(x.cpu().pow(2).mean(-1, keepdim=True) + 1e-6) * (1 + scale.cpu()) + shift.cpu()
     assert rel_l2(out, exp) < 5e-3
 
 
-def test_norm_modulate_probe():
-    rows, hidden = 513, 256
+@pytest.mark.parametrize("rows,hidden", [(513, 256), (975, 2048), (301, 3072)])
+def test_norm_modulate_probe(rows, hidden):
+    """warp-per-row (hidden < 1024) and CTA-per-row (wide rows) variants."""
     g = torch.Generator(device=dev).manual_seed(3)
     x = torch.randn(rows, hidden, device=dev, generator=g)
     prev = torch.randn(rows, hidden, device=dev, generator=g)
