@@ -39,6 +39,16 @@ UNIT = "denoise_steps/s"
 PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
+def traffic(kind):
+    """ncu-measured DRAM bytes per launch of the dominant kernel class (profiles/r01_traffic.json)."""
+    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    if not os.path.exists(p):
+        return None, None
+    with open(p) as fh:
+        d = json.load(fh).get(kind)
+    return (d["dram_bytes_per_launch"], d) if d else (None, None)
+
+
 def peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -327,9 +337,13 @@ def run_ours(args):
     if dom in tensor_kinds:
         ach = d["work"] / (d["ms"] / 1e3) / 1e12
         peak = pk["bf16_tflops_sustained"]
+        tb, tinfo = traffic(dom)
         roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": None, "peak_source": f"{pk_src} bf16 sustained",
+                "frac": ach / peak, "traffic": tb, "peak_source": f"{pk_src} bf16 sustained",
                 "share_of_step": d["ms"] / tot_ms}
+        if tinfo:
+            roof["traffic_note"] = (f"{tinfo['kernel']}: {tb / 1e6:.1f} MB DRAM per launch vs "
+                                    f"{tinfo['algorithmic_bytes_per_launch'] / 1e6:.1f} MB algorithmic ({tinfo['source']})")
     else:
         ach = d["work"] / (d["ms"] / 1e3) / 1e9
         peak = pk["hbm_gbs"]
@@ -366,7 +380,8 @@ def run_ours(args):
                                             "memory over NVLink; device barrier)" if sp.exchange == "p2p" else
                                             " all_to_all")) if sp else None,
                        "l2": "inputs larger than L2 (4.3 GB of bf16 weights streamed per step)",
-                       "cuda_graphs": bool(args.graph)},
+                       "cuda_graphs": bool(args.graph),
+                       "pdl": os.environ.get("AQB_PDL", "1") != "0"},
             "cache_off": {"value": value_off, "unit": UNIT, "ms_per_video": ms_off / max(1, args.steps)},
             "cache_speedup_measured": value / value_off,
             "schedule": sched_on.as_string(),

@@ -113,7 +113,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ OutMaps om, Params p) {
   using C = Cfg<D>;
-  if (!gate_open(p.run_flag, p.run_if)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t* sQ = base + C::kOffQ;
@@ -155,8 +154,12 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // the prologue above overlapped the previous kernel (PDL); inputs only after this
+  pdl_trigger();
+  const bool run = gate_open(p.run_flag, p.run_if);
 
-  if (warp == 0) {
+  if (!run) {
+  } else if (warp == 0) {
     // ------------------------------------------------------------ producer
     setmaxnreg_dec<kCtrlRegs>();
     if (lane == 0) {
@@ -436,6 +439,8 @@ __global__ void __launch_bounds__(kThreads, 1)
 // Split-KV combine: one warp per (row, head); lane owns 4 of the D columns.
 //   O = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M),  M = max_s lse_s
 __global__ void __launch_bounds__(256) attn_combine_kernel(Params p) {
+  pdl_wait();
+  pdl_trigger();
   if (!gate_open(p.run_flag, p.run_if)) return;
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
@@ -552,11 +557,11 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     memset(&om, 0, sizeof(om));
   }
   dim3 grid((p.seq_q + 2 * BQ - 1) / (2 * BQ), p.heads, p.splits);
-  kern<<<grid, kThreads, smem, stream>>>(tq, tk, tv, om, p);
+  AQB_CUDA_TRY(launch_pdl(kern, grid, dim3(kThreads), smem, stream, tq, tk, tv, om, p));
   AQB_LAUNCH_CHECK();
   if (p.splits > 1) {
     const int64_t warps = static_cast<int64_t>(p.seq_q) * p.heads;
-    attn_combine_kernel<<<unsigned((warps * 32 + 255) / 256), 256, 0, stream>>>(p);
+    AQB_CUDA_TRY(launch_pdl(attn_combine_kernel, dim3(unsigned((warps * 32 + 255) / 256)), dim3(256), 0, stream, p));
     AQB_LAUNCH_CHECK();
   }
   return AQB_OK;

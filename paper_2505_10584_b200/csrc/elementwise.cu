@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
                                                        int64_t ldy, int64_t rows, float eps, int kind,
                                                        float* __restrict__ prev, float* __restrict__ partials,
                                                        const int32_t* flag, int32_t run_if) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   if (!gate_open(flag, run_if)) return;
   const int lane = threadIdx.x & 31;
   const int64_t row = static_cast<int64_t>(blockIdx.x) * 8 + (threadIdx.x >> 5);
@@ -130,6 +132,8 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
                                                                int64_t ldy, int64_t rows, float eps, int kind,
                                                                float* __restrict__ prev, float* __restrict__ partials,
                                                                const int32_t* flag, int32_t run_if) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   if (!gate_open(flag, run_if)) return;
   __shared__ float red[NW];
   constexpr int T = NW * 32, H = T * 16;
@@ -197,6 +201,8 @@ __global__ void __launch_bounds__(256) qk_norm_rope_kernel(
     const float* __restrict__ qw, const float* __restrict__ kw, float eps, const float* __restrict__ rcos,
     const float* __restrict__ rsin, int64_t rope_row0, int64_t rope_rows, T* dst, int64_t g_stride,
     int64_t r_stride, int64_t w_stride, int hpg, int parts, int norm_parts, const int32_t* flag, int32_t run_if) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   if (!gate_open(flag, run_if)) return;
   constexpr int NP = (D / 2 + 31) / 32;  // pairs per lane
   const int lane = threadIdx.x & 31;
@@ -254,6 +260,8 @@ __global__ void __launch_bounds__(256) gemv_kernel(const __nv_bfloat16* __restri
                                                    const float* __restrict__ t, const float* __restrict__ b,
                                                    const float* __restrict__ add, float* __restrict__ y, int64_t n,
                                                    int k, int in_silu) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   extern __shared__ float xs[];
   const float tv = t ? __ldg(t) : 0.f;
   const int half = k / 2;
@@ -293,6 +301,8 @@ __global__ void __launch_bounds__(256) gemv_kernel(const __nv_bfloat16* __restri
 }
 
 __global__ void add_bcast_kernel(float* out, const float* a, int64_t period, const float* b, int64_t n) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
        i += static_cast<int64_t>(gridDim.x) * blockDim.x)
     out[i] = a[i % period] + b[i];
@@ -300,6 +310,8 @@ __global__ void add_bcast_kernel(float* out, const float* a, int64_t period, con
 
 // ------------------------------------------------------- diffusion cache
 __global__ void __launch_bounds__(1024) rel_l1_reduce_kernel(const float* partials, int64_t rows, float* sums) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   __shared__ float sd[32], sp[32];
   float d = 0.f, p = 0.f;
   for (int64_t i = threadIdx.x; i < rows; i += 1024) {
@@ -319,6 +331,8 @@ __global__ void __launch_bounds__(1024) rel_l1_reduce_kernel(const float* partia
 
 __global__ void cache_decide_kernel(const float* sums, int32_t* state, float thr, int warmup, int total,
                                     int force_last, int32_t* flags_out, float* rel_out) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   const int s = state[0] + 1;
   float* accp = reinterpret_cast<float*>(state + 2);
   float acc = *accp;
@@ -345,6 +359,8 @@ __global__ void cache_decide_kernel(const float* sums, int32_t* state, float thr
 
 __global__ void cache_offset_kernel(float* x, int64_t ldx, float* off, int64_t rows, int hidden, int mode,
                                     const int32_t* flag, int32_t run_if) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   if (!gate_open(flag, run_if)) return;
   const int64_t n4 = rows * (hidden / 4);
   const int h4 = hidden / 4;
@@ -366,6 +382,8 @@ __global__ void cache_offset_kernel(float* x, int64_t ldx, float* off, int64_t r
 }
 
 __global__ void step_scalars_kernel(const float* ts, const float* dts, int32_t* idx, float* cur, int mode) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   const int i = *idx;
   cur[0] = ts[i];
   cur[1] = dts[i];
@@ -377,6 +395,8 @@ __global__ void step_scalars_kernel(const float* ts, const float* dts, int32_t* 
 // (a temporal window of a longer latent: MultiDiffusion clips).
 __global__ void patchify_kernel(const float* lat, float* tok, __nv_bfloat16* tokb, int C, int T, int H, int W, int pt,
                                 int ph, int pw, int Tl, int t0) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   const int F = pt * ph * pw * C;
   const int64_t n = static_cast<int64_t>(T) * H * W * F;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -398,6 +418,8 @@ __global__ void patchify_kernel(const float* lat, float* tok, __nv_bfloat16* tok
 
 __global__ void unpatchify_kernel(const float* tok, float* lat, int C, int T, int H, int W, int pt, int ph, int pw,
                                   int Tl, int t0) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   const int F = pt * ph * pw * C;
   const int64_t n = static_cast<int64_t>(T) * H * W * F;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -418,6 +440,8 @@ __global__ void unpatchify_kernel(const float* tok, float* lat, int C, int T, in
 // src [P, rows, width] -> dst [rows, P*width] (16-byte units)
 __global__ void heads_to_seq_kernel(const uint4* src, int64_t rows, int P, int w16, uint4* dst, int64_t ld16,
                                     const int32_t* flag, int32_t run_if) {
+  pdl_wait();  // PDL: predecessor's writes visible from here
+  pdl_trigger();
   if (!gate_open(flag, run_if)) return;
   const int64_t n = rows * P * w16;
   for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < n;
@@ -457,9 +481,9 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
     switch (hidden / 512) {
 #define NMR_CASE(NW)                                                                                               \
   case NW:                                                                                                         \
-    norm_mod_row_kernel<NW, OutT><<<unsigned(rows), NW * 32, 0, s>>>(x, ldx, shift, scale, yb, ldy, rows, eps,     \
+    AQB_CUDA_TRY(launch_pdl(norm_mod_row_kernel<NW, OutT>, dim3(unsigned(rows)), dim3(NW * 32), 0, s, x, ldx, shift, scale, yb, ldy, rows, eps,     \
                                                                      norm_kind, probe_prev, probe_partials,        \
-                                                                     run_flag, run_if);                            \
+                                                                     run_flag, run_if));                            \
     AQB_LAUNCH_CHECK();                                                                                            \
     return AQB_OK;
       NMR_CASE(2) NMR_CASE(3) NMR_CASE(4) NMR_CASE(5) NMR_CASE(6) NMR_CASE(7) NMR_CASE(8)
@@ -469,8 +493,8 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
   }
 #define NM_CASE(NV)                                                                                          \
   case NV:                                                                                                   \
-    norm_mod_kernel<NV, OutT><<<grid, 256, 0, s>>>(x, ldx, shift, scale, yb, ldy, rows, eps, norm_kind,      \
-                                                   probe_prev, probe_partials, run_flag, run_if);            \
+    AQB_CUDA_TRY(launch_pdl(norm_mod_kernel<NV, OutT>, dim3(grid), dim3(256), 0, s, x, ldx, shift, scale, yb, ldy, rows, eps, norm_kind,      \
+                                                   probe_prev, probe_partials, run_flag, run_if));            \
     break;
   switch (hidden / 128) {
     NM_CASE(1) NM_CASE(2) NM_CASE(3) NM_CASE(4) NM_CASE(6) NM_CASE(8) NM_CASE(12) NM_CASE(16) NM_CASE(20)
@@ -522,10 +546,10 @@ static int qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t h
   auto dp = reinterpret_cast<T*>(dst);
 #define QK_CASE(D)                                                                                                \
   case D:                                                                                                         \
-    qk_norm_rope_kernel<D, T><<<grid, 256, 0, s>>>(sp, ld_src, rows, heads, head_begin, head_count, q_w, k_w,     \
+    AQB_CUDA_TRY(launch_pdl(qk_norm_rope_kernel<D, T>, dim3(grid), dim3(256), 0, s, sp, ld_src, rows, heads, head_begin, head_count, q_w, k_w,     \
                                                    eps, rope_cos, rope_sin, rope_row0, rope_rows, dp,             \
                                                    dst_group_stride, dst_row_stride, dst_which_stride, hpg, parts, \
-                                                   norm_parts, run_flag, run_if);                                 \
+                                                   norm_parts, run_flag, run_if));                                 \
     break;
   switch (head_dim) {
     QK_CASE(32) QK_CASE(64) QK_CASE(128) QK_CASE(256)
@@ -568,8 +592,7 @@ extern "C" int aqb_gemv(const void* w, const float* x, const float* t, const flo
   int64_t g = (n + 7) / 8;
   const int64_t cap = static_cast<int64_t>(sm_count()) * 8;
   if (g > cap) g = cap;
-  gemv_kernel<<<static_cast<int>(g), 256, k * sizeof(float), reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const __nv_bfloat16*>(w), x, t, b, add, y, n, static_cast<int>(k), in_silu);
+  AQB_CUDA_TRY(launch_pdl(gemv_kernel, dim3(static_cast<int>(g)), dim3(256), k * sizeof(float), reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<const __nv_bfloat16*>(w), x, t, b, add, y, n, static_cast<int>(k), in_silu));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
@@ -577,14 +600,14 @@ extern "C" int aqb_gemv(const void* w, const float* x, const float* t, const flo
 extern "C" int aqb_add_bcast(float* out, const float* a, int64_t period, const float* b, int64_t n, void* stream) {
   AQB_CHECK_ARG(out && a && b && period >= 1, "add_bcast: bad args");
   if (n <= 0) return AQB_OK;
-  add_bcast_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(out, a, period, b, n);
+  AQB_CUDA_TRY(launch_pdl(add_bcast_kernel, dim3(grid_for(n, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), out, a, period, b, n));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
 
 extern "C" int aqb_rel_l1_reduce(const float* partials, int64_t rows, float* sums, void* stream) {
   AQB_CHECK_ARG(partials && sums && rows >= 1, "rel_l1_reduce: bad args");
-  rel_l1_reduce_kernel<<<1, 1024, 0, reinterpret_cast<cudaStream_t>(stream)>>>(partials, rows, sums);
+  AQB_CUDA_TRY(launch_pdl(rel_l1_reduce_kernel, dim3(1), dim3(1024), 0, reinterpret_cast<cudaStream_t>(stream), partials, rows, sums));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
@@ -593,8 +616,8 @@ extern "C" int aqb_cache_decide(const float* sums, int32_t* state, float thresho
                                 int32_t total_steps, int32_t force_last, int32_t* flags_out, float* rel_out,
                                 void* stream) {
   AQB_CHECK_ARG(sums && state && total_steps >= 1, "cache_decide: bad args");
-  cache_decide_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(sums, state, threshold, warmup, total_steps,
-                                                                            force_last, flags_out, rel_out);
+  AQB_CUDA_TRY(launch_pdl(cache_decide_kernel, dim3(1), dim3(1), 0, reinterpret_cast<cudaStream_t>(stream), sums, state, threshold, warmup, total_steps,
+                                                                            force_last, flags_out, rel_out));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
@@ -603,8 +626,7 @@ extern "C" int aqb_cache_offset(float* x, int64_t ldx, float* off, int64_t rows,
                                 const int32_t* run_flag, int32_t run_if, void* stream) {
   AQB_CHECK_ARG(x && off && hidden % 4 == 0 && ldx % 4 == 0 && mode >= 0 && mode <= 2, "cache_offset: bad args");
   if (rows <= 0) return AQB_OK;
-  cache_offset_kernel<<<grid_for(rows * hidden / 4, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      x, ldx, off, rows, hidden, mode, run_flag, run_if);
+  AQB_CUDA_TRY(launch_pdl(cache_offset_kernel, dim3(grid_for(rows * hidden / 4, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), x, ldx, off, rows, hidden, mode, run_flag, run_if));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
@@ -612,7 +634,7 @@ extern "C" int aqb_cache_offset(float* x, int64_t ldx, float* off, int64_t rows,
 extern "C" int aqb_step_scalars(const float* ts, const float* dts, int32_t* idx, float* cur, int32_t mode,
                                 void* stream) {
   AQB_CHECK_ARG(ts && dts && idx && cur, "step_scalars: null pointer");
-  step_scalars_kernel<<<1, 1, 0, reinterpret_cast<cudaStream_t>(stream)>>>(ts, dts, idx, cur, mode);
+  AQB_CUDA_TRY(launch_pdl(step_scalars_kernel, dim3(1), dim3(1), 0, reinterpret_cast<cudaStream_t>(stream), ts, dts, idx, cur, mode));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
@@ -623,8 +645,7 @@ extern "C" int aqb_patchify(const float* lat, float* tok, void* tok_bf16, int32_
   AQB_CHECK_ARG(lat && tok && C > 0 && T > 0 && H > 0 && W > 0 && pt > 0 && ph > 0 && pw > 0, "patchify: bad args");
   AQB_CHECK_ARG(frame_offset >= 0 && frame_offset + T * pt <= lat_frames, "patchify: frame window out of range");
   const int64_t n = static_cast<int64_t>(C) * T * H * W * pt * ph * pw;
-  patchify_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      lat, tok, reinterpret_cast<__nv_bfloat16*>(tok_bf16), C, T, H, W, pt, ph, pw, lat_frames, frame_offset);
+  AQB_CUDA_TRY(launch_pdl(patchify_kernel, dim3(grid_for(n, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), lat, tok, reinterpret_cast<__nv_bfloat16*>(tok_bf16), C, T, H, W, pt, ph, pw, lat_frames, frame_offset));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
@@ -634,9 +655,9 @@ extern "C" int aqb_unpatchify(const float* tok, float* lat, int32_t C, int32_t T
   AQB_CHECK_ARG(lat && tok && C > 0 && T > 0 && H > 0 && W > 0 && pt > 0 && ph > 0 && pw > 0, "unpatchify: bad args");
   AQB_CHECK_ARG(frame_offset >= 0 && frame_offset + T * pt <= lat_frames, "unpatchify: frame window out of range");
   const int64_t n = static_cast<int64_t>(C) * T * H * W * pt * ph * pw;
-  unpatchify_kernel<<<grid_for(n, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(tok, lat, C, T, H, W, pt,
+  AQB_CUDA_TRY(launch_pdl(unpatchify_kernel, dim3(grid_for(n, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), tok, lat, C, T, H, W, pt,
                                                                                            ph, pw, lat_frames,
-                                                                                           frame_offset);
+                                                                                           frame_offset));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
@@ -647,8 +668,7 @@ extern "C" int aqb_heads_to_seq(const void* src, int64_t rows, int32_t P, int32_
                 "heads_to_seq: bad args");
   if (rows <= 0) return AQB_OK;
   const int w16 = width / 8;
-  heads_to_seq_kernel<<<grid_for(rows * P * w16, 256), 256, 0, reinterpret_cast<cudaStream_t>(stream)>>>(
-      reinterpret_cast<const uint4*>(src), rows, P, w16, reinterpret_cast<uint4*>(dst), ld_dst / 8, run_flag, run_if);
+  AQB_CUDA_TRY(launch_pdl(heads_to_seq_kernel, dim3(grid_for(rows * P * w16, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), reinterpret_cast<const uint4*>(src), rows, P, w16, reinterpret_cast<uint4*>(dst), ld_dst / 8, run_flag, run_if));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }

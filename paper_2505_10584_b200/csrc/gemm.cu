@@ -374,7 +374,6 @@ template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                 const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ PeerMaps pm, Params p) {
-  if (!gate_open(p.run_flag, p.run_if)) return;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(base);
@@ -411,8 +410,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nk = (p.K + BK - 1) / BK;
+  // the prologue above overlaps the previous kernel's tail (PDL); inputs only after this
+  pdl_wait();
+  pdl_trigger();
+  const bool run = gate_open(p.run_flag, p.run_if);
 
-  if (warp == 0) {
+  if (!run) {
+  } else if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -488,7 +492,6 @@ template <int BN, int STAGES, int EPI>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     gemm2_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                  const __grid_constant__ CUtensorMap tma_o, const __grid_constant__ PeerMaps pm, Params p) {
-  if (!gate_open(p.run_flag, p.run_if)) return;
   constexpr int BNH = BN / 2;  // W rows per CTA
   constexpr int kABytes = BM * BK * 2, kBBytes = BNH * BK * 2;
   extern __shared__ uint8_t smem_raw[];
@@ -531,8 +534,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nk = (p.K + BK - 1) / BK;
+  pdl_wait();  // prologue overlapped the previous kernel (PDL); inputs only after this
+  pdl_trigger();
+  const bool run = gate_open(p.run_flag, p.run_if);
 
-  if (warp == 0) {
+  if (!run) {
+  } else if (warp == 0) {
     if (lane == 0) {
       int stage = 0;
       uint32_t phase = 0;
@@ -629,7 +636,7 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, 
   } else {
     grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
   }
-  kern<<<grid, kThreads, smem, stream>>>(ta, tb, to, pm, p);
+  AQB_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, stream, ta, tb, to, pm, p));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }

@@ -1,6 +1,7 @@
 // Host helpers: error reporting, TMA descriptor encoding, device properties.
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 
 #include "host.cuh"
@@ -30,6 +31,15 @@ int sm_count() {
     cached[dev] = n > 0 ? n : 148;
   }
   return cached[dev];
+}
+
+bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("AQB_PDL");
+    on = (e && e[0] == '0') ? 0 : 1;
+  }
+  return on == 1;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {

@@ -10,6 +10,7 @@
 
 #include <cstdarg>
 #include <mutex>
+#include <utility>
 
 #include "../../include/aqb.h"
 
@@ -40,6 +41,26 @@ const char* last_error();
   } while (0)
 
 int sm_count();
+
+// Launch with programmatic stream serialization (PDL) unless AQB_PDL=0: the kernel
+// must call pdl_wait() before reading anything the previous kernel wrote.
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                       Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // Encode a bf16 tensor map with 128B swizzle.  dims/strides innermost first;
 // strides in bytes for dims 1..rank-1.  Returns 0 or a negative status.

@@ -354,6 +354,14 @@ AQB_DEV uint32_t pack_bf16(float a, float b) {
 
 // Run-gate for device-decided cache skipping: a kernel runs iff flag == nullptr
 // or *flag == run_if.  Read once per CTA by every thread (same address, L1/L2 hit).
+// Programmatic dependent launch (PDL): kernels launched with launch_pdl() may start
+// while the previous kernel in the stream drains; pdl_wait() blocks until that
+// kernel has completed and its writes are visible, so it must precede every read of
+// a predecessor's output (including run_flag).  pdl_trigger() lets the next kernel
+// start launching.  Both are no-ops for ordinary launches.
+AQB_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+AQB_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 AQB_DEV bool gate_open(const int32_t* flag, int32_t run_if) {
   return flag == nullptr || __ldg(flag) == run_if;
 }
