@@ -180,28 +180,37 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs the loop (all values warp-uniform) and one elected lane
+    // issues each tcgen05 op: issuing from a `lane == 0` branch made the compiler
+    // wrap every MMA in a uniform-register waterfall loop (R2UR/ELECT/BRA.U.ANY), and
+    // at one 128x128x16 MMA per ~68 cycles that issue cost throttled the tensor pipe.
     setmaxnreg_dec<kCtrlRegs>();
-    if (lane == 0) {
+    {
       constexpr uint32_t kIdescS = idesc_bf16(BQ, BKV, 0, 0);  // Q, K both K-major
       constexpr uint32_t kIdescO = idesc_bf16(BQ, D, 0, 1);    // P K-major, V MN-major
-      const uint32_t q_addr = smem_u32(sQ), kv_addr = smem_u32(sKV);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      const uint32_t q_addr = __shfl_sync(0xffffffffu, smem_u32(sQ), 0);
+      const uint32_t kv_addr = __shfl_sync(0xffffffffu, smem_u32(sKV), 0);
       auto issue_qk = [&](int t, int stage) {
         const uint32_t a0 = q_addr + t * C::kQBytes, b0 = kv_addr + stage * C::kKVBytes;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
           const uint32_t off = (kk >> 2) * (BQ * 128) + (kk & 3) * 32;
-          umma_bf16_ss(tmem + t * 128, smem_desc(a0 + off, 0, 1024), smem_desc(b0 + off, 0, 1024), kIdescS, kk > 0);
+          const uint64_t da = smem_desc(a0 + off, 0, 1024), db = smem_desc(b0 + off, 0, 1024);
+          if (elect_one()) umma_bf16_ss(tm + t * 128, da, db, kIdescS, kk > 0);
         }
       };
-      auto issue_pv = [&](int t, int stage, bool acc, int kk0, int kk1) {
+      auto issue_pv = [&](int t, int stage, bool acc) {
         // A = P_t straight from TMEM (columns 64..127 of S_t, bf16 pairs), B = V (MN-major smem)
-        const uint32_t a0 = tmem + t * 128 + kPCol, b0 = kv_addr + stage * C::kKVBytes;
+        const uint32_t a0 = tm + t * 128 + kPCol, b0 = kv_addr + stage * C::kKVBytes;
 #pragma unroll
-        for (int kk = kk0; kk < kk1; ++kk) {
-          const uint32_t boff = kk * 16 * 128;  // 16 keys x 128 B rows
-          umma_bf16_ts(tmem + 256 + t * D, a0 + kk * 8, smem_desc(b0 + boff, BKV * 128, 1024), kIdescO,
-                       (acc || kk > 0) ? 1u : 0u);
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint64_t db = smem_desc(b0 + kk * 16 * 128, BKV * 128, 1024);  // 16 keys x 128 B rows
+          if (elect_one()) umma_bf16_ts(tm + 256 + t * D, a0 + kk * 8, db, kIdescO, (acc || kk > 0) ? 1u : 0u);
         }
+      };
+      auto commit = [&](uint64_t* bar) {
+        if (elect_one()) umma_commit(bar);
       };
       mbar_wait(q_full, 0);
       tc_fence_after();
@@ -215,24 +224,24 @@ __global__ void __launch_bounds__(kThreads, 1)
           mbar_wait(kv_full + iv % C::NS, (iv / C::NS) & 1);
           mbar_wait(p_full + 0, (j - 1) & 1);
           tc_fence_after();
-          issue_pv(0, iv % C::NS, j > 1, 0, BKV / 16);
-          umma_commit(o_ready + 0);
+          issue_pv(0, iv % C::NS, j > 1);
+          commit(o_ready + 0);
         }
         if (j < nkv) {
           issue_qk(0, ik % C::NS);
-          umma_commit(s_full + 0);
+          commit(s_full + 0);
         }
         if (j > 0) {
           mbar_wait(p_full + 1, (j - 1) & 1);
           tc_fence_after();
-          issue_pv(1, iv % C::NS, j > 1, 0, BKV / 16);
-          umma_commit(o_ready + 1);
-          umma_commit(kv_empty + iv % C::NS);
+          issue_pv(1, iv % C::NS, j > 1);
+          commit(o_ready + 1);
+          commit(kv_empty + iv % C::NS);
         }
         if (j < nkv) {
           issue_qk(1, ik % C::NS);
-          umma_commit(s_full + 1);
-          umma_commit(kv_empty + ik % C::NS);
+          commit(s_full + 1);
+          commit(kv_empty + ik % C::NS);
         }
       }
     }
