@@ -162,21 +162,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else if (warp == 0) {
     // ------------------------------------------------------------ producer
     setmaxnreg_dec<kCtrlRegs>();
-    if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * C::kQBytes);
-      for (int t = 0; t < 2; ++t)
-        for (int c = 0; c < C::kBoxes; ++c)
+    // warp-wide loop, one elected lane per TMA op (keeps operands in uniform registers)
+    if (elect_one()) mbar_arrive_expect_tx(q_full, 2 * C::kQBytes);
+    for (int t = 0; t < 2; ++t)
+      for (int c = 0; c < C::kBoxes; ++c)
+        if (elect_one())
           tma_load_3d(sQ + t * C::kQBytes + c * (BQ * 128), &tq, q_full, c * 64, head, q0 + t * BQ, kEvictFirst);
-      for (int i = 0; i < 2 * nkv; ++i) {
-        const int s = i % C::NS;
-        const uint32_t ph = (i / C::NS) & 1;
-        mbar_wait(kv_empty + s, ph ^ 1);
-        mbar_arrive_expect_tx(kv_full + s, C::kKVBytes);
-        const CUtensorMap* m = (i & 1) ? &tv : &tk;
-        const int row = (j0 + (i >> 1)) * BKV;
-        for (int c = 0; c < C::kBoxes; ++c)
+    for (int i = 0; i < 2 * nkv; ++i) {
+      const int s = i % C::NS;
+      const uint32_t ph = (i / C::NS) & 1;
+      mbar_wait(kv_empty + s, ph ^ 1);
+      if (elect_one()) mbar_arrive_expect_tx(kv_full + s, C::kKVBytes);
+      const CUtensorMap* m = (i & 1) ? &tv : &tk;
+      const int row = (j0 + (i >> 1)) * BKV;
+      for (int c = 0; c < C::kBoxes; ++c)
+        if (elect_one())
           tma_load_3d(sKV + s * C::kKVBytes + c * (BKV * 128), m, kv_full + s, c * 64, head, row, kEvictLast);
-      }
     }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer

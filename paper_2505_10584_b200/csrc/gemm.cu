@@ -417,48 +417,49 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   if (!run) {
   } else if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        int mb, nb;
-        tile_coords(p, t, mb, nb);
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
-          mbar_arrive_expect_tx(full + stage, (BM + BN) * BK * 2);
-          tma_load_2d(sa + stage * BM * BK, &tma_a, full + stage, kb * BK, mb * BM);
-          tma_load_2d(sb + stage * BN * BK, &tma_b, full + stage, kb * BK, nb * BN);
-          if (++stage == STAGES) stage = 0, phase ^= 1;
-        }
+    // producer and MMA issuer run warp-wide with one elected lane per TMA / tcgen05 op,
+    // so descriptors stay in uniform registers (no per-op waterfall loop)
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(empty + stage, phase ^ 1);
+        if (elect_one()) mbar_arrive_expect_tx(full + stage, (BM + BN) * BK * 2);
+        if (elect_one()) tma_load_2d(sa + stage * BM * BK, &tma_a, full + stage, kb * BK, mb * BM);
+        if (elect_one()) tma_load_2d(sb + stage * BN * BK, &tma_b, full + stage, kb * BK, nb * BN);
+        if (++stage == STAGES) stage = 0, phase ^= 1;
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t kIdesc = idesc_bf16(BM, BN, 0, 0);
-      int stage = 0;
-      uint32_t phase = 0;
-      int acc = 0;
-      uint32_t acc_phase = 0;
-      for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
-        mbar_wait(tempty + acc, acc_phase ^ 1);
+    constexpr uint32_t kIdesc = idesc_bf16(BM, BN, 0, 0);
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      mbar_wait(tempty + acc, acc_phase ^ 1);
+      tc_fence_after();
+      const uint32_t d = tm + acc * BN;
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(full + stage, phase);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(full + stage, phase);
-          tc_fence_after();
-          const uint32_t a0 = smem_u32(sa + stage * BM * BK);
-          const uint32_t b0 = smem_u32(sb + stage * BN * BK);
+        const uint32_t a0 = smem_u32(sa + stage * BM * BK);
+        const uint32_t b0 = smem_u32(sb + stage * BN * BK);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            // K-major SW128: +32 B per 16-element K step inside the 128 B swizzle row.
-            umma_bf16_ss(d, smem_desc(a0 + 32 * k, 0, 1024), smem_desc(b0 + 32 * k, 0, 1024), kIdesc, (kb | k) != 0);
-          umma_commit(empty + stage);
-          if (++stage == STAGES) stage = 0, phase ^= 1;
+        for (int k = 0; k < BK / 16; ++k) {
+          // K-major SW128: +32 B per 16-element K step inside the 128 B swizzle row.
+          const uint64_t da = smem_desc(a0 + 32 * k, 0, 1024), db = smem_desc(b0 + 32 * k, 0, 1024);
+          if (elect_one()) umma_bf16_ss(d, da, db, kIdesc, (kb | k) != 0);
         }
-        umma_commit(tfull + acc);
-        acc ^= 1;
-        if (acc == 0) acc_phase ^= 1;
+        if (elect_one()) umma_commit(empty + stage);
+        if (++stage == STAGES) stage = 0, phase ^= 1;
       }
+      if (elect_one()) umma_commit(tfull + acc);
+      acc ^= 1;
+      if (acc == 0) acc_phase ^= 1;
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
@@ -540,27 +541,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 
   if (!run) {
   } else if (warp == 0) {
-    if (lane == 0) {
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int t = cluster; t < p.num_tiles; t += nclusters) {
-        int mb, nb;
-        tile_coords(p, t, mb, nb);
-        for (int kb = 0; kb < nk; ++kb) {
-          mbar_wait(empty + stage, phase ^ 1);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int t = cluster; t < p.num_tiles; t += nclusters) {
+      int mb, nb;
+      tile_coords(p, t, mb, nb);
+      for (int kb = 0; kb < nk; ++kb) {
+        mbar_wait(empty + stage, phase ^ 1);
+        if (elect_one())
           tma_load_2d_pair(sa + stage * kABytes, &tma_a, full + stage, kb * BK, mb * (2 * BM) + rank * BM);
-          tma_load_2d_pair(sb + stage * kBBytes, &tma_b, full + stage, kb * BK, nb * BN + rank * BNH);
+        if (elect_one()) tma_load_2d_pair(sb + stage * kBBytes, &tma_b, full + stage, kb * BK, nb * BN + rank * BNH);
+        if (elect_one()) {
           if (leader)
             mbar_arrive_expect_tx(full + stage, 2 * (kABytes + kBBytes));
           else
             mbar_arrive_cluster(full + stage, 0);
-          if (++stage == STAGES) stage = 0, phase ^= 1;
         }
+        if (++stage == STAGES) stage = 0, phase ^= 1;
       }
     }
   } else if (warp == 1) {
-    if (leader && lane == 0) {
+    if (leader) {
       constexpr uint32_t kIdesc = idesc_bf16(2 * BM, BN, 0, 0);
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
@@ -568,19 +571,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       for (int t = cluster; t < p.num_tiles; t += nclusters) {
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
-        const uint32_t d = tmem + acc * BN;
+        const uint32_t d = tm + acc * BN;
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
           const uint32_t a0 = smem_u32(sa + stage * kABytes);
           const uint32_t b0 = smem_u32(sb + stage * kBBytes);
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k)
-            umma_bf16_pair(d, smem_desc(a0 + 32 * k, 0, 1024), smem_desc(b0 + 32 * k, 0, 1024), kIdesc, (kb | k) != 0);
-          umma_commit_pair(empty + stage);
+          for (int k = 0; k < BK / 16; ++k) {
+            const uint64_t da = smem_desc(a0 + 32 * k, 0, 1024), db = smem_desc(b0 + 32 * k, 0, 1024);
+            if (elect_one()) umma_bf16_pair(d, da, db, kIdesc, (kb | k) != 0);
+          }
+          if (elect_one()) umma_commit_pair(empty + stage);
           if (++stage == STAGES) stage = 0, phase ^= 1;
         }
-        umma_commit_pair(tfull + acc);
+        if (elect_one()) umma_commit_pair(tfull + acc);
         acc ^= 1;
         if (acc == 0) acc_phase ^= 1;
       }
