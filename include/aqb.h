@@ -139,7 +139,8 @@ int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t head
  * q + h*q_head_stride with row stride ldq (likewise K, V, O).  bf16 in/out;
  * f32 softmax statistics.  head_dim in {32, 64, 128}.  seq_kv >= 1.
  * Split-KV (few heads x queries vs. 148 SMs, e.g. Ulysses' A/P heads):
- * kv_splits = 0 picks the split count (aqb_attention_splits), 1 disables it;
+ * kv_splits = 0 picks a plan (the wave-quantisation tail, or every tile when
+ * few, split aqb_attention_splits ways), 1 disables it, s > 1 splits all tiles;
  * the partials (f32 O/l + log2-sum-exp2 per row) go to `workspace`
  * (aqb_attention_workspace_bytes) and a combine pass writes O.  Automatic
  * splitting silently stays at 1 split without enough workspace.
@@ -150,7 +151,12 @@ int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const v
                       int32_t head_dim, float softmax_scale, int32_t kv_splits, void* workspace,
                       int64_t workspace_bytes, const int32_t* run_flag, int32_t run_if, void* stream);
 int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
+/* tiles (head x 256 queries) the automatic plan runs in one pass; the rest split
+ * aqb_attention_splits ways (wave-quantisation tail, or all tiles when few) */
+int aqb_attention_whole_tiles(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
+/* workspace for any plan of <= kv_splits splits, and for the automatic plan */
 int64_t aqb_attention_workspace_bytes(int64_t seq_q, int32_t heads, int32_t head_dim, int32_t kv_splits);
+int64_t aqb_attention_auto_workspace_bytes(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
 
 /* Ulysses "AlltoAll after attention" fused into the attention epilogue
  * (comm.py:65-96 costs it): output row r < text_row0 of head h

@@ -27,6 +27,10 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <vector>
 
 #include "host.cuh"
 #include "ptx.cuh"
@@ -84,9 +88,15 @@ struct Params {
   int seq_q, seq_kv, heads, head_dim;
   float scale_log2;
   OutMap out;
-  int splits, kv_blocks_per_split;  // split-KV: blockIdx.z = split; partials go to opart/lse
-  float* opart;                     // [splits][heads][seq_q][head_dim] f32 (O / l of the split)
-  float* lse;                       // [splits][heads][seq_q] f32, log2-sum-exp2 of the split
+  // Work plan (1-D grid; tile = head * q_pairs + 256-query block): CTAs [0, n_whole)
+  // run tiles 0..n_whole-1 over all KV blocks; every later tile is split over KV
+  // into `splits` CTAs of kv_blocks_per_split blocks (the wave-quantisation tail,
+  // or every tile when heads x Q blocks leave SMs idle).  Split partials go to
+  // opart/lse in compact order ((tile - n_whole) * splits + split) * 256 + row.
+  int q_pairs, n_whole;
+  int splits, kv_blocks_per_split;
+  float* opart;                     // [tail tiles][splits][256][part_d] f32 (O / l of the split)
+  float* lse;                       // [tail tiles][splits][256] f32, log2-sum-exp2 of the split
   int part_d;                       // row stride of opart (the kernel's D)
   const int32_t* run_flag;
   int32_t run_if;
@@ -127,11 +137,15 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_ready + 2);
 
   const uint32_t warp = warp_idx(), lane = lane_idx();
-  const int head = blockIdx.y;
-  const int q0 = blockIdx.x * (2 * BQ);
-  const int split = blockIdx.z;
-  const int j0 = split * p.kv_blocks_per_split;  // first KV block of this split
-  const int nkv = min((p.seq_kv + BKV - 1) / BKV - j0, p.kv_blocks_per_split);
+  const int cta = blockIdx.x;
+  const bool whole = cta < p.n_whole;
+  const int tile = whole ? cta : p.n_whole + (cta - p.n_whole) / p.splits;
+  const int split = whole ? 0 : (cta - p.n_whole) % p.splits;
+  const int head = tile / p.q_pairs;
+  const int q0 = (tile % p.q_pairs) * (2 * BQ);
+  const int nkv_all = (p.seq_kv + BKV - 1) / BKV;
+  const int j0 = whole ? 0 : split * p.kv_blocks_per_split;  // first KV block of this CTA
+  const int nkv = whole ? nkv_all : min(nkv_all - j0, p.kv_blocks_per_split);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
@@ -362,8 +376,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int row = q0 + t * BQ + r;
     const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
     const bool live = row < p.seq_q;
-    if (p.splits > 1) {
-      const int64_t prow = (static_cast<int64_t>(split) * p.heads + head) * p.seq_q + row;
+    if (!whole) {
+      const int64_t prow = (static_cast<int64_t>(tile - p.n_whole) * p.splits + split) * (2 * BQ) + t * BQ + r;
       if (live) p.lse[prow] = m_run * c + __log2f(l_run);
       float* orow = p.opart + prow * D;
 #pragma unroll 1
@@ -446,7 +460,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-// Split-KV combine: one warp per (row, head); lane owns 4 of the D columns.
+// Split-KV combine: one warp per row of a split tile; lane owns 4 of the D columns.
 //   O = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M),  M = max_s lse_s
 __global__ void __launch_bounds__(256) attn_combine_kernel(Params p) {
   pdl_wait();
@@ -454,21 +468,26 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(Params p) {
   if (!gate_open(p.run_flag, p.run_if)) return;
   const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (w >= static_cast<int64_t>(p.seq_q) * p.heads) return;
-  const int head = int(w % p.heads);
-  const int64_t row = w / p.heads;
-  const int64_t plane = static_cast<int64_t>(p.heads) * p.seq_q;
-  const int64_t base = static_cast<int64_t>(head) * p.seq_q + row;
+  const int64_t tail = static_cast<int64_t>(p.q_pairs) * p.heads - p.n_whole;
+  if (w >= tail * (2 * BQ)) return;
+  const int64_t tl = w / (2 * BQ);
+  const int r = int(w % (2 * BQ));
+  const int tile = p.n_whole + int(tl);
+  const int head = tile / p.q_pairs;
+  const int64_t row = int64_t(tile % p.q_pairs) * (2 * BQ) + r;
+  if (row >= p.seq_q) return;
+  const int64_t base = tl * p.splits * (2 * BQ) + r;  // split s at base + s * 256
   float mx = -INFINITY;
-  for (int s = 0; s < p.splits; ++s) mx = fmaxf(mx, p.lse[s * plane + base]);
+  for (int s = 0; s < p.splits; ++s) mx = fmaxf(mx, p.lse[base + s * (2 * BQ)]);
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   float den = 0.f;
   const int D = p.head_dim, PD = p.part_d;
   for (int s = 0; s < p.splits; ++s) {
-    const float wt = exp2f(p.lse[s * plane + base] - mx);
+    const int64_t pr = base + s * (2 * BQ);
+    const float wt = exp2f(p.lse[pr] - mx);
     den += wt;
     if (lane * 4 < D) {
-      const float4 v = *reinterpret_cast<const float4*>(p.opart + (s * plane + base) * PD + lane * 4);
+      const float4 v = *reinterpret_cast<const float4*>(p.opart + pr * PD + lane * 4);
       acc.x += wt * v.x, acc.y += wt * v.y, acc.z += wt * v.z, acc.w += wt * v.w;
     }
   }
@@ -478,23 +497,76 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(Params p) {
   for_each_out(p.out, head, row, [&](__nv_bfloat16* orow) { *reinterpret_cast<uint2*>(orow + lane * 4) = pk; });
 }
 
-// KV splits for a launch: minimise waves x (KV blocks per split + fixed cost)
-// plus the combine pass's traffic, expressed in KV-block units (~2.3 us per
-// 256-query block on one SM at ~1.1 PFLOP/s device-wide).
-int choose_splits(int64_t seq_q, int64_t seq_kv, int heads, int head_dim) {
-  const int nkv = int((seq_kv + BKV - 1) / BKV);
-  const int64_t units = ((seq_q + 2 * BQ - 1) / (2 * BQ)) * heads;
-  const double sms = sm_count();
-  double best = 1e30;
-  int bs = 1;
-  for (int s = 1; s <= 16 && s <= nkv / 2 + (s == 1); ++s) {
-    const int per = (nkv + s - 1) / s;
-    const double waves = std::ceil(double(units) * s / sms);
-    double t = waves * (per + 2.0);
-    if (s > 1) t += double(s) * seq_q * heads * (head_dim * 4 + 4) * 2.0 / 5e12 / 2.3e-6 + 1.0;
-    if (t < best * 0.95) best = t, bs = s;
+// Work plan for one launch (see Params): which tiles run whole and how the rest
+// split over KV.  Candidates — no split; every tile split s ways; the last
+// `tail` tiles split s ways for the tails left by 0..3 whole waves — are
+// list-scheduled onto one CTA slot per SM in launch order (the order the
+// hardware hands out CTAs), each CTA costing its KV blocks + 2 (Q load,
+// epilogue); the combine pass costs its partial traffic in KV-block units
+// (~2.3 us per 256-query KV block on one SM).  Lowest makespan wins, a split
+// plan only if it saves > 5%.
+struct Plan {
+  int n_whole, splits, per;
+};
+
+static double simulate(int64_t n_whole, int64_t tail, int s, int per, int nkv, int slots) {
+  // n_whole CTAs of nkv + 2, then tail * s CTAs of (per or the remainder) + 2
+  std::vector<double> fin(slots, 0.0);
+  auto put = [&](double len) {
+    auto it = std::min_element(fin.begin(), fin.end());
+    *it += len;
+  };
+  for (int64_t i = 0; i < n_whole && i < 4 * slots; ++i) put(nkv + 2.0);
+  if (n_whole > 4 * slots) {  // long uniform prefix: whole waves, then the remainder
+    const int64_t rest = n_whole - 4 * slots;
+    for (auto& f : fin) f += double(rest / slots) * (nkv + 2.0);
+    for (int64_t i = 0; i < rest % slots; ++i) put(nkv + 2.0);
   }
-  return bs;
+  for (int64_t t = 0; t < tail; ++t)
+    for (int j = 0; j < s; ++j) put(std::min(per, nkv - j * per) + 2.0);
+  return *std::max_element(fin.begin(), fin.end());
+}
+
+static Plan choose_plan_uncached(int64_t seq_q, int64_t seq_kv, int heads, int head_dim) {
+  const int nkv = int((seq_kv + BKV - 1) / BKV);
+  const int64_t tiles = ((seq_q + 2 * BQ - 1) / (2 * BQ)) * heads;
+  const int slots = sm_count();
+  Plan best{int(tiles), 1, nkv};
+  const double t1 = simulate(tiles, 0, 1, nkv, nkv, slots);
+  double bt = t1;
+  auto consider = [&](int64_t tail, int s) {
+    const int per = (nkv + s - 1) / s;
+    s = (nkv + per - 1) / per;  // no empty split
+    if (s < 2 || tail <= 0 || tail > tiles || tail * s > 64 * int64_t(slots)) return;
+    double t = simulate(tiles - tail, tail, s, per, nkv, slots);
+    t += double(s) * tail * (2 * BQ) * (head_dim * 4 + 4) * 2.0 / 5e12 / 2.3e-6 + 1.0;
+    if (t < bt && t < t1 * 0.95) bt = t, best = Plan{int(tiles - tail), s, per};
+  };
+  for (int s = 2; s <= 16 && s <= nkv; ++s) {
+    consider(tiles, s);
+    const int64_t rem = tiles % slots;
+    for (int k = 0; k < 4; ++k) consider(rem + int64_t(k) * slots, s);
+  }
+  return best;
+}
+
+Plan choose_plan(int64_t seq_q, int64_t seq_kv, int heads, int head_dim) {
+  static std::mutex mu;
+  static std::map<std::tuple<int64_t, int64_t, int, int>, Plan> cache;
+  const auto key = std::make_tuple(seq_q, seq_kv, heads, head_dim);
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = cache.find(key);
+  if (it != cache.end()) return it->second;
+  const Plan pl = choose_plan_uncached(seq_q, seq_kv, heads, head_dim);
+  if (cache.size() < 4096) cache.emplace(key, pl);
+  return pl;
+}
+
+static int64_t split_ws_bytes(int64_t tail_tiles, int splits, int head_dim) {
+  if (splits <= 1 || tail_tiles <= 0) return 0;
+  const int64_t rows = tail_tiles * splits * (2 * BQ);
+  const int64_t d = head_dim <= 64 ? 64 : 128;
+  return ((rows + 63) / 64 * 64 + rows * d) * 4;
 }
 
 // Output TMA maps for p.out (see OutMaps).
@@ -560,17 +632,18 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     configured = true;
   }
   OutMaps om;
-  if (p.splits == 1) {
+  if (p.n_whole > 0) {
     int rc = make_out_maps(p, om);
     if (rc) return rc;
   } else {
     memset(&om, 0, sizeof(om));
   }
-  dim3 grid((p.seq_q + 2 * BQ - 1) / (2 * BQ), p.heads, p.splits);
-  AQB_CUDA_TRY(launch_pdl(kern, grid, dim3(kThreads), smem, stream, tq, tk, tv, om, p));
+  const int64_t tiles = static_cast<int64_t>(p.q_pairs) * p.heads;
+  const int64_t ctas = p.n_whole + (tiles - p.n_whole) * p.splits;
+  AQB_CUDA_TRY(launch_pdl(kern, dim3(unsigned(ctas)), dim3(kThreads), smem, stream, tq, tk, tv, om, p));
   AQB_LAUNCH_CHECK();
-  if (p.splits > 1) {
-    const int64_t warps = static_cast<int64_t>(p.seq_q) * p.heads;
+  if (p.n_whole < tiles) {
+    const int64_t warps = (tiles - p.n_whole) * (2 * BQ);
     AQB_CUDA_TRY(launch_pdl(attn_combine_kernel, dim3(unsigned((warps * 32 + 255) / 256)), dim3(256), 0, stream, p));
     AQB_LAUNCH_CHECK();
   }
@@ -595,29 +668,36 @@ static int run(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t l
   AQB_CHECK_ARG(qhs % 8 == 0 && khs % 8 == 0 && vhs % 8 == 0 && om.o_head_stride % 8 == 0,
                 "attention: head strides must be 16B aligned");
   const int nkv = int((seq_kv + BKV - 1) / BKV);
-  int splits = kv_splits > 0 ? kv_splits : choose_splits(seq_q, seq_kv, heads, head_dim);
-  splits = std::min(splits, nkv);
-  const int per = (nkv + splits - 1) / splits;
-  splits = (nkv + per - 1) / per;  // no empty split
-  if (splits > 1) {
-    const int64_t need = aqb_attention_workspace_bytes(seq_q, heads, head_dim, splits);
-    if (workspace == nullptr || workspace_bytes < need) {
-      AQB_CHECK_ARG(kv_splits <= 1, "attention: workspace of %lld B needed for %d splits", (long long)need, splits);
-      splits = 1;  // automatic choice without (enough) workspace: one pass
-    }
+  const int64_t tiles = ((seq_q + 2 * BQ - 1) / (2 * BQ)) * heads;
+  AQB_CHECK_ARG(tiles * std::min(kv_splits > 0 ? kv_splits : 16, nkv) < (1ll << 31), "attention: grid too large");
+  Plan plan;
+  if (kv_splits > 0) {  // forced: every tile split the same way (1 = one pass)
+    const int s = std::min(int(kv_splits), nkv);
+    const int per = (nkv + s - 1) / s;
+    plan = Plan{0, (nkv + per - 1) / per, per};
+    if (plan.splits == 1) plan = Plan{int(tiles), 1, nkv};
+  } else {
+    plan = choose_plan(seq_q, seq_kv, heads, head_dim);
+  }
+  const int64_t need = split_ws_bytes(tiles - plan.n_whole, plan.splits, head_dim);
+  if (need > 0 && (workspace == nullptr || workspace_bytes < need)) {
+    AQB_CHECK_ARG(kv_splits <= 1, "attention: workspace of %lld B needed for %d splits", (long long)need, plan.splits);
+    plan = Plan{int(tiles), 1, nkv};  // automatic choice without (enough) workspace: one pass
   }
   Params p{};
   p.seq_q = int(seq_q), p.seq_kv = int(seq_kv), p.heads = heads, p.head_dim = head_dim;
   p.scale_log2 = softmax_scale * 1.4426950408889634f;
   p.out = om;
-  p.splits = splits;
-  p.kv_blocks_per_split = splits > 1 ? per : nkv;
+  p.q_pairs = int((seq_q + 2 * BQ - 1) / (2 * BQ));
+  p.n_whole = plan.n_whole;
+  p.splits = plan.splits;
+  p.kv_blocks_per_split = plan.per;
   p.part_d = head_dim <= 64 ? 64 : 128;
-  if (splits > 1) {
+  if (plan.n_whole < tiles) {
     float* ws = reinterpret_cast<float*>(workspace);
     p.lse = ws;
-    const int64_t lse_elems = (static_cast<int64_t>(splits) * heads * seq_q + 63) / 64 * 64;
-    p.opart = ws + lse_elems;
+    const int64_t rows = (tiles - plan.n_whole) * plan.splits * (2 * BQ);
+    p.opart = ws + (rows + 63) / 64 * 64;
   }
   p.run_flag = run_flag, p.run_if = run_if;
   if (head_dim == 128) return launch<128>(q, ldq, qhs, k, ldk, khs, v, ldv, vhs, p, s);
@@ -628,14 +708,22 @@ static int run(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t l
 }  // namespace aqb
 
 extern "C" int64_t aqb_attention_workspace_bytes(int64_t seq_q, int32_t heads, int32_t head_dim, int32_t kv_splits) {
-  if (kv_splits <= 1) return 0;
-  const int64_t rows = static_cast<int64_t>(kv_splits) * heads * seq_q;
-  const int64_t d = head_dim <= 64 ? 64 : head_dim;
-  return ((rows + 63) / 64 * 64 + rows * d) * 4;
+  // any plan with <= kv_splits splits (the all-tiles-split plan is the largest)
+  return aqb::attn::split_ws_bytes((seq_q + 255) / 256 * heads, kv_splits, head_dim);
+}
+
+extern "C" int64_t aqb_attention_auto_workspace_bytes(int64_t seq_q, int64_t seq_kv, int32_t heads,
+                                                      int32_t head_dim) {
+  const aqb::attn::Plan pl = aqb::attn::choose_plan(seq_q, seq_kv, heads, head_dim);
+  return aqb::attn::split_ws_bytes((seq_q + 255) / 256 * heads - pl.n_whole, pl.splits, head_dim);
 }
 
 extern "C" int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim) {
-  return aqb::attn::choose_splits(seq_q, seq_kv, heads, head_dim);
+  return aqb::attn::choose_plan(seq_q, seq_kv, heads, head_dim).splits;
+}
+
+extern "C" int aqb_attention_whole_tiles(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim) {
+  return aqb::attn::choose_plan(seq_q, seq_kv, heads, head_dim).n_whole;
 }
 
 extern "C" int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const void* k, int64_t ldk,

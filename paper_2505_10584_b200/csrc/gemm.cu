@@ -21,7 +21,7 @@
 // Epilogue: per 128-byte-wide column chunk (32 fp32 / 64 bf16 columns), each
 // thread (= one TMEM lane = one row) pulls its accumulators with tcgen05.ld,
 // the residual chunk (gate*residual) arrives by TMA into a 128B-swizzled smem
-// buffer, the thread combines bias / GeLU / gate / residual in registers,
+// buffer (requested several chunks ahead, across tile boundaries), the thread combines bias / GeLU / gate / residual in registers,
 // writes the result back to the swizzled buffer (conflict-free 16 B accesses),
 // and one thread TMA-stores the chunk.  All global traffic is TMA (coalesced);
 // the two smem buffers alternate so a chunk's store overlaps the next chunk.
@@ -45,6 +45,9 @@ constexpr int kAuxBuf = 128 * 64;   // bf16 copy of a gate*residual chunk: 128 r
 struct Params {
   int M, N, K;
   int num_m, num_n, num_tiles, group_m;
+  // Work units: tiles [0, n_full) are whole BN-wide tiles; each later tile runs as two
+  // BN/2-wide units (pair kernel, BN = 256), so a short last wave takes half as long.
+  int n_full, num_units;
   void* out;
   int64_t ldo;
   const float* bias;
@@ -72,6 +75,7 @@ struct Params {
 constexpr int kMaxPeers = 8;
 struct PeerMaps {
   CUtensorMap m[kMaxPeers];
+  CUtensorMap bh;  // W with a BN/4-row box: the half-width tail units of the pair kernel
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int& nb) {
@@ -82,6 +86,20 @@ __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int
   const int r = t - g * per_group;
   mb = first_m + r % gsz;
   nb = r / gsz;
+}
+
+// Unit u -> (M block, first column, width): whole tiles first, then half-width tail units.
+template <int BN>
+__device__ __forceinline__ void unit_coords(const Params& p, int u, int& mb, int& col0, int& width) {
+  int nb;
+  if (u < p.n_full) {
+    tile_coords(p, u, mb, nb);
+    col0 = nb * BN, width = BN;
+  } else {
+    const int v = u - p.n_full;
+    tile_coords(p, p.n_full + (v >> 1), mb, nb);
+    col0 = nb * BN + (v & 1) * (BN / 2), width = BN / 2;
+  }
 }
 
 __device__ __forceinline__ float4 ld_f4(const float* p) {
@@ -127,15 +145,42 @@ __device__ __forceinline__ void euler_chunk(const Params& p, int row, int col0, 
 
 // Per-CTA epilogue state (warps 4-7 only).
 struct EpiState {
-  uint8_t* buf;      // kEpiBufs(EPI) x kEpiBuf, 1024-aligned (gate*residual: + 2 x kAuxBuf bf16 copies)
+  uint8_t* buf;      // epi_bufs x kEpiBuf, 1024-aligned (gate*residual: + 2 x kAuxBuf bf16 copies)
   uint64_t* bar;     // one mbarrier per buffer (residual TMA loads)
-  uint32_t chunk;    // chunks processed by this CTA (buffer / phase bookkeeping)
+  uint32_t chunk;    // chunks processed by this CTA (buffer / phase bookkeeping; aux buffers)
+  // gate*residual residual stream: chunk index space idx = tile_iter * (BN / 32) + c, where
+  // tile_iter counts this CTA's tiles (first_tile, first_tile + tile_stride, ...)
+  int first_tile, tile_stride, tile_m, row_off;
+  uint32_t tiles_done;   // tile_iter of the tile being drained
+  uint32_t issued;       // residual chunks requested so far (idx < issued)
+  uint32_t phase_bits;   // per-buffer mbarrier parity (loads happen only for valid chunks)
 };
 
-// gate*residual keeps three buffers so the residual of chunk c+1 streams in
-// while chunk c is combined; the store-only epilogues need two.
-template <int EPI>
-constexpr int epi_bufs() { return EPI == AQB_EPI_GATE_RES ? 3 : 2; }
+constexpr int kSmemMax = 232448;
+constexpr int kFixedRes = 2 * kAuxBuf + 1024 + 256;  // aux copies + alignment + barriers
+
+template <int BN, bool PAIR>
+constexpr int stage_bytes() { return (BM + (PAIR ? BN / 2 : BN)) * BK * 2; }
+
+// gate*residual streams the f32 residual through NB buffers, requested NB-2 chunks
+// ahead (across tile boundaries); every buffer left after the pipeline stages is used,
+// up to 8.  Measured: 5 buffers / 4 stages was no faster than 3 / 5 on the K = H
+// projections and 10% slower on K = 4H, so res_stages keeps the stages.  The
+// store-only epilogues need two.
+template <int BN, int STAGES, bool PAIR, int EPI>
+constexpr int epi_bufs() {
+  if (EPI != AQB_EPI_GATE_RES) return 2;
+  const int n = (kSmemMax - kFixedRes - STAGES * stage_bytes<BN, PAIR>()) / kEpiBuf;
+  return n > 8 ? 8 : n;
+}
+
+// pipeline stages of the gate*residual variant: the most that leave >= 3 residual buffers
+template <int BN, int STAGES, bool PAIR>
+constexpr int res_stages() {
+  for (int s = STAGES; s > 3; --s)
+    if ((kSmemMax - kFixedRes - s * stage_bytes<BN, PAIR>()) / kEpiBuf >= 3) return s;
+  return 3;
+}
 
 template <int EPI>
 constexpr int aux_bytes() { return EPI == AQB_EPI_GATE_RES ? 2 * kAuxBuf : 0; }
@@ -143,32 +188,49 @@ constexpr int aux_bytes() { return EPI == AQB_EPI_GATE_RES ? 2 * kAuxBuf : 0; }
 template <int EPI>
 constexpr int epi_cols() { return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES) ? 32 : 64; }
 
-// Residual prefetch for the first chunk of a tile, issued before the
-// accumulator wait so its latency hides behind the tile's MMAs.
-template <int EPI>
-__device__ __forceinline__ void epilogue_prologue(const Params& p, const CUtensorMap* tmo, EpiState& es, int row0,
-                                                  int col_base, bool leader_thread) {
+// Request residual chunk `idx` (leader thread; no-op past the last tile / column N).
+template <int BN, int NB>
+__device__ __forceinline__ void res_request(const Params& p, const CUtensorMap* tmo, EpiState& es, uint32_t idx) {
+  constexpr int CPT = BN / 32;
+  const int u = es.first_tile + int(idx / CPT) * es.tile_stride;
+  if (u >= p.num_units) return;
+  int mb, col0, width;
+  unit_coords<BN>(p, u, mb, col0, width);
+  const int c = int(idx % CPT) * 32;
+  const int col = col0 + c;
+  if (c >= width || col >= p.N) return;
+  const uint32_t b = idx % NB;
+  bulk_wait_read<1>();  // buffer b was last TMA-stored from two chunks ago
+  mbar_arrive_expect_tx(es.bar + b, kEpiBuf);
+  tma_load_2d(es.buf + b * kEpiBuf, tmo, es.bar + b, col, mb * es.tile_m + es.row_off, kEvictFirst);
+}
+
+// Residual prefetch before the first tile's accumulator wait, so the stream's
+// start-up latency hides behind the first tile's MMAs.
+template <int EPI, int BN, int NB>
+__device__ __forceinline__ void epilogue_prologue(const Params& p, const CUtensorMap* tmo, EpiState& es,
+                                                  bool leader_thread) {
   if constexpr (EPI == AQB_EPI_GATE_RES) {
-    if (leader_thread && col_base < p.N) {
-      const uint32_t b = es.chunk % 3;
-      bulk_wait_read<2>();  // buffer b was last stored 3 chunks ago
-      mbar_arrive_expect_tx(es.bar + b, kEpiBuf);
-      tma_load_2d(es.buf + b * kEpiBuf, tmo, es.bar + b, col_base, row0, kEvictFirst);
+    if (es.issued == 0) {
+      if (leader_thread)
+        for (uint32_t i = 0; i < NB - 2; ++i) res_request<BN, NB>(p, tmo, es, i);
+      es.issued = NB - 2;
     }
   }
 }
 
 // One accumulator tile (this CTA's 128 rows x BN columns starting at col_base).
-template <int EPI, int BN>
+template <int EPI, int BN, int NB>
 __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap* tmo, const PeerMaps* pm, EpiState& es,
-                                              uint32_t tacc, int row0, int col_base, uint32_t q, uint32_t lane) {
+                                              uint32_t tacc, int row0, int col_base, int width, uint32_t q,
+                                              uint32_t lane) {
   const int r = q * 32 + lane;           // row within the CTA tile (= TMEM lane)
   const uint32_t lane_off = (q * 32) << 16;
   const bool leader_thread = (q == 0 && lane == 0);
   if constexpr (EPI == AQB_EPI_EULER) {
 #pragma unroll 1
     for (int c = 0; c < BN; c += 32) {
-      if (col_base + c >= p.N) break;
+      if (c >= width || col_base + c >= p.N) break;
       uint32_t u[32];
       tmem_ld32(tacc + c + lane_off, u);
       tmem_wait_ld();
@@ -182,7 +244,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 #pragma unroll 1
     for (int hc = 0; hc < BN; hc += 128) {
       const int colh = col_base + hc;
-      if (colh >= p.N) break;
+      if (hc >= width || colh >= p.N) break;
       float v[128];
       {
         uint32_t u[32];
@@ -262,22 +324,24 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       }
     }
   } else {
-    constexpr int NB = epi_bufs<EPI>();
     constexpr int CW = epi_cols<EPI>();  // columns per 128-byte chunk
 #pragma unroll 1
     for (int c = 0; c < BN; c += CW) {
       const int col0 = col_base + c;
-      if (col0 >= p.N) break;  // uniform over the 128 epilogue threads
-      const uint32_t b = es.chunk % NB;
+      uint32_t b;
+      if constexpr (EPI == AQB_EPI_GATE_RES) {
+        // chunk idx's residual was requested NB-2 chunks ago; request idx + NB - 2
+        const uint32_t idx = es.tiles_done * (BN / 32) + c / 32;
+        if (leader_thread && idx + NB - 2 >= es.issued) res_request<BN, NB>(p, tmo, es, idx + NB - 2);
+        es.issued = idx + NB - 1;
+        if (c >= width || col0 >= p.N) continue;  // uniform over the 128 epilogue threads
+        b = idx % NB;
+      } else {
+        if (c >= width || col0 >= p.N) break;  // uniform over the 128 epilogue threads
+        b = es.chunk % NB;
+      }
       uint8_t* buf = es.buf + b * kEpiBuf;
       if constexpr (EPI == AQB_EPI_GATE_RES) {
-        // this chunk's residual was requested one chunk (or one tile) ago; request the next one
-        if (leader_thread && c + CW < BN && col0 + CW < p.N) {
-          const uint32_t bn = (es.chunk + 1) % NB;
-          bulk_wait_read<1>();  // buffer bn was last stored two chunks ago
-          mbar_arrive_expect_tx(es.bar + bn, kEpiBuf);
-          tma_load_2d(es.buf + bn * kEpiBuf, tmo, es.bar + bn, col0 + CW, row0, kEvictFirst);
-        }
       } else {
         // buffer b was last read by the TMA store issued NB chunks ago
         if (leader_thread) bulk_wait_read<NB - 1>();
@@ -312,7 +376,8 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           if (leader_thread) bulk_wait_read<1>();
           named_bar_sync(1, 128);
         }
-        mbar_wait(es.bar + b, (es.chunk / NB) & 1);
+        mbar_wait(es.bar + b, (es.phase_bits >> b) & 1);
+        es.phase_bits ^= 1u << b;
         const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
         const uint32_t arow = smem_u32(abuf) + r * 64, asw = (r >> 1) & 3;
 #pragma unroll
@@ -361,12 +426,13 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       }
       ++es.chunk;
     }
+    if constexpr (EPI == AQB_EPI_GATE_RES) ++es.tiles_done;
   }
 }
 
 template <int BN, int STAGES, bool PAIR, int EPI>
 constexpr int smem_bytes() {
-  return STAGES * (BM + (PAIR ? BN / 2 : BN)) * BK * 2 + epi_bufs<EPI>() * kEpiBuf + aux_bytes<EPI>() +
+  return STAGES * (BM + (PAIR ? BN / 2 : BN)) * BK * 2 + epi_bufs<BN, STAGES, PAIR, EPI>() * kEpiBuf + aux_bytes<EPI>() +
          1024 /*align*/ + 256 /*bars*/;
 }
 
@@ -379,12 +445,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __nv_bfloat16* sa = reinterpret_cast<__nv_bfloat16*>(base);
   __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(base + STAGES * BM * BK * 2);
   uint8_t* ebuf = base + STAGES * (BM + BN) * BK * 2;
-  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf + aux_bytes<EPI>());
+  constexpr int NB = epi_bufs<BN, STAGES, false, EPI>();
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + NB * kEpiBuf + aux_bytes<EPI>());
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* ebar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 3);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + NB);
 
   constexpr uint32_t kTmemCols = 2 * BN;
   const uint32_t warp = warp_idx(), lane = lane_idx();
@@ -401,7 +468,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, 4);
     }
-    for (int b = 0; b < 3; ++b) mbar_init(ebar + b, 1);
+    for (int b = 0; b < NB; ++b) mbar_init(ebar + b, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -421,7 +488,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     // so descriptors stay in uniform registers (no per-op waterfall loop)
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int t = blockIdx.x; t < p.num_units; t += gridDim.x) {  // 1-CTA: every unit is a whole tile
       int mb, nb;
       tile_coords(p, t, mb, nb);
       for (int kb = 0; kb < nk; ++kb) {
@@ -439,7 +506,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int t = blockIdx.x; t < p.num_units; t += gridDim.x) {
       mbar_wait(tempty + acc, acc_phase ^ 1);
       tc_fence_after();
       const uint32_t d = tm + acc * BN;
@@ -463,16 +530,16 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
-    EpiState es{ebuf, ebar, 0};
+    EpiState es{ebuf, ebar, 0, int(blockIdx.x), int(gridDim.x), BM, 0, 0, 0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+    for (int t = blockIdx.x; t < p.num_units; t += gridDim.x) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
-      epilogue_prologue<EPI>(p, &tma_o, es, mb * BM, nb * BN, q == 0 && lane == 0);
+      epilogue_prologue<EPI, BN, NB>(p, &tma_o, es, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      epilogue_tile<EPI, BN>(p, &tma_o, &pm, es, tmem + acc * BN, mb * BM, nb * BN, q, lane);
+      epilogue_tile<EPI, BN, NB>(p, &tma_o, &pm, es, tmem + acc * BN, mb * BM, nb * BN, BN, q, lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
@@ -500,12 +567,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sa = base;
   uint8_t* sb = base + STAGES * kABytes;
   uint8_t* ebuf = base + STAGES * (kABytes + kBBytes);
-  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + epi_bufs<EPI>() * kEpiBuf + aux_bytes<EPI>());
+  constexpr int NB = epi_bufs<BN, STAGES, true, EPI>();
+  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + NB * kEpiBuf + aux_bytes<EPI>());
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* ebar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + 3);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + NB);
 
   constexpr uint32_t kTmemCols = 2 * BN;
   const uint32_t warp = warp_idx(), lane = lane_idx();
@@ -525,7 +593,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(tfull + a, 1);   // multicast MMA commit
       mbar_init(tempty + a, 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
     }
-    for (int b = 0; b < 3; ++b) mbar_init(ebar + b, 1);
+    for (int b = 0; b < NB; ++b) mbar_init(ebar + b, 1);
     fence_barrier_init();
   }
   cluster_sync();
@@ -543,17 +611,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 0) {
     int stage = 0;
     uint32_t phase = 0;
-    for (int t = cluster; t < p.num_tiles; t += nclusters) {
-      int mb, nb;
-      tile_coords(p, t, mb, nb);
+    for (int u = cluster; u < p.num_units; u += nclusters) {
+      int mb, col0, width;
+      unit_coords<BN>(p, u, mb, col0, width);
+      const bool half = width != BN;
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(empty + stage, phase ^ 1);
         if (elect_one())
           tma_load_2d_pair(sa + stage * kABytes, &tma_a, full + stage, kb * BK, mb * (2 * BM) + rank * BM);
-        if (elect_one()) tma_load_2d_pair(sb + stage * kBBytes, &tma_b, full + stage, kb * BK, nb * BN + rank * BNH);
+        if (elect_one()) {
+          if (half)
+            tma_load_2d_pair(sb + stage * kBBytes, &pm.bh, full + stage, kb * BK, col0 + rank * (BNH / 2));
+          else
+            tma_load_2d_pair(sb + stage * kBBytes, &tma_b, full + stage, kb * BK, col0 + rank * BNH);
+        }
         if (elect_one()) {
           if (leader)
-            mbar_arrive_expect_tx(full + stage, 2 * (kABytes + kBBytes));
+            mbar_arrive_expect_tx(full + stage, 2 * (kABytes + (half ? kBBytes / 2 : kBBytes)));
           else
             mbar_arrive_cluster(full + stage, 0);
         }
@@ -563,12 +637,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   } else if (warp == 1) {
     if (leader) {
       constexpr uint32_t kIdesc = idesc_bf16(2 * BM, BN, 0, 0);
+      constexpr uint32_t kIdescHalf = idesc_bf16(2 * BM, BN / 2, 0, 0);
       const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int t = cluster; t < p.num_tiles; t += nclusters) {
+      for (int u = cluster; u < p.num_units; u += nclusters) {
+        const uint32_t idesc = u < p.n_full ? kIdesc : kIdescHalf;
         mbar_wait(tempty + acc, acc_phase ^ 1);
         tc_fence_after();
         const uint32_t d = tm + acc * BN;
@@ -580,7 +656,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
 #pragma unroll
           for (int k = 0; k < BK / 16; ++k) {
             const uint64_t da = smem_desc(a0 + 32 * k, 0, 1024), db = smem_desc(b0 + 32 * k, 0, 1024);
-            if (elect_one()) umma_bf16_pair(d, da, db, kIdesc, (kb | k) != 0);
+            if (elect_one()) umma_bf16_pair(d, da, db, idesc, (kb | k) != 0);
           }
           if (elect_one()) umma_commit_pair(empty + stage);
           if (++stage == STAGES) stage = 0, phase ^= 1;
@@ -592,16 +668,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;
-    EpiState es{ebuf, ebar, 0};
+    EpiState es{ebuf, ebar, 0, cluster, nclusters, 2 * BM, int(rank) * BM, 0, 0, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = cluster; t < p.num_tiles; t += nclusters) {
-      int mb, nb;
-      tile_coords(p, t, mb, nb);
-      epilogue_prologue<EPI>(p, &tma_o, es, mb * (2 * BM) + rank * BM, nb * BN, q == 0 && lane == 0);
+    for (int u = cluster; u < p.num_units; u += nclusters) {
+      int mb, col0, width;
+      unit_coords<BN>(p, u, mb, col0, width);
+      epilogue_prologue<EPI, BN, NB>(p, &tma_o, es, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
-      epilogue_tile<EPI, BN>(p, &tma_o, &pm, es, tmem + acc * BN, mb * (2 * BM) + rank * BM, nb * BN, q, lane);
+      epilogue_tile<EPI, BN, NB>(p, &tma_o, &pm, es, tmem + acc * BN, mb * (2 * BM) + rank * BM, col0, width, q,
+                                 lane);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -637,9 +714,9 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, 
   int grid;
   if (PAIR) {
     const int pairs = sm_count() / 2;
-    grid = 2 * (p.num_tiles < pairs ? p.num_tiles : pairs);
+    grid = 2 * (p.num_units < pairs ? p.num_units : pairs);
   } else {
-    grid = p.num_tiles < sm_count() ? p.num_tiles : sm_count();
+    grid = p.num_units < sm_count() ? p.num_units : sm_count();
   }
   AQB_CUDA_TRY(launch_pdl(kern, dim3(grid), dim3(kThreads), smem, stream, ta, tb, to, pm, p));
   AQB_LAUNCH_CHECK();
@@ -649,11 +726,8 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, 
 template <int BN, int STAGES, bool PAIR>
 int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, const PeerMaps& pm,
                  const Params& p, cudaStream_t s) {
-  // one pipeline stage makes room for the third gate*residual buffer
-  // gate*residual: 3 f32 buffers + 2 bf16 aux buffers; drop pipeline stages until it fits
-  constexpr int kStageBytes = (PAIR ? BM + BN / 2 : BM + BN) * BK * 2;
-  constexpr int kFixed = 3 * kEpiBuf + 2 * kAuxBuf + 1024 + 256;
-  constexpr int kResStages = (232448 - kFixed) / kStageBytes < STAGES ? (232448 - kFixed) / kStageBytes : STAGES;
+  // gate*residual trades pipeline stages for residual buffers (see epi_bufs / res_stages)
+  constexpr int kResStages = res_stages<BN, STAGES, PAIR>();
   switch (epi) {
     case AQB_EPI_BF16: return launch<BN, STAGES, AQB_EPI_BF16, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16, PAIR>(ta, tb, to, pm, p, s);
@@ -670,6 +744,25 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
 // bytes each SM loads.  AQB_GEMM_VARIANT=1cta256|1cta128|2cta256|2cta128
 // forces one (benchmarking).
 enum Variant { V1_256 = 0, V1_128, V2_256, V2_128 };
+
+// Tiles of a pair-kernel launch (BN = 256) that run as two half-width units: the
+// partial last wave when it fills at most half the CTA pairs (it then takes half a
+// tile's time instead of a whole one).  Needs at least one whole wave: a launch of
+// only half-width units streams 1.5x the operand bytes per FLOP from L2 and measured
+// no faster (975x2048x8192: -8%).  AQB_GEMM_HALF_TAIL=0 disables (benchmarking).
+// Measured (B200, L2 flushed): 7800x2048x2048 1162 -> 1302 TFLOP/s, x8192 1428 -> 1588,
+// 7800x8192x2048 GeLU 1588 -> 1692, 7800x6144x2048 1534 -> 1585, 975x6144x2048 685 -> 825.
+static int half_tail_tiles(int tiles, bool pair, int bn) {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("AQB_GEMM_HALF_TAIL");
+    enabled = (e && !strcmp(e, "0")) ? 0 : 1;
+  }
+  if (!enabled || !pair || bn != 256) return 0;
+  const int pairs = sm_count() / 2;
+  const int r = tiles % pairs;
+  return (tiles > pairs && r > 0 && 2 * r <= pairs) ? r : 0;
+}
 
 static int pick_variant(int64_t m, int64_t n, int64_t k) {
   static int forced = -2;
@@ -690,7 +783,8 @@ static int pick_variant(int64_t m, int64_t n, int64_t k) {
   int bv = V2_256;
   for (auto& c : cs) {
     const double tiles = double((m + c.tm - 1) / c.tm) * double((n + c.tn - 1) / c.tn);
-    const double waves = std::ceil(tiles / (sms / c.ctas));
+    double waves = std::ceil(tiles / (sms / c.ctas));
+    if (half_tail_tiles(int(tiles), c.ctas == 2, c.tn) > 0) waves -= 0.5;
     const double rows = c.tm / c.ctas;                        // A rows per SM
     const double bytes = (rows + double(c.tn) / c.ctas) * 2;  // per SM per k
     const double mma = rows * c.tn / 4096.0 * 0.5;            // cycles per SM per k
@@ -710,8 +804,11 @@ namespace gemm {
 // Shared host path: A/W tensor maps, variant choice, tile bookkeeping, launch.
 static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m, int64_t n, int64_t k, int epilogue,
                Params& p, const CUtensorMap& to, int variant, cudaStream_t s, const PeerMaps* pm_in = nullptr) {
-  static const PeerMaps kNoPeers{};
-  const PeerMaps& pm = pm_in ? *pm_in : kNoPeers;
+  PeerMaps pm;
+  if (pm_in)
+    pm = *pm_in;
+  else
+    memset(&pm, 0, sizeof(pm));
   const bool pair = variant == V2_256 || variant == V2_128;
   const int bn = (variant == V1_256 || variant == V2_256) ? 256 : 128;
   const int tile_m = pair ? 2 * BM : BM;
@@ -735,6 +832,17 @@ static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m
   p.num_n = int((n + bn - 1) / bn);
   p.num_tiles = p.num_m * p.num_n;
   p.group_m = 16;
+  p.n_full = p.num_tiles;
+  const int tail = half_tail_tiles(p.num_tiles, pair, bn);
+  if (tail > 0) {  // the last `tail` tiles run as two half-width units each
+    uint64_t dims[2] = {uint64_t(k), uint64_t(n)};
+    uint64_t strides[1] = {uint64_t(ldw) * 2};
+    uint32_t box[2] = {BK, uint32_t(bn / 4)};
+    int rc = make_tmap_bf16(&pm.bh, w, 2, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    p.n_full = p.num_tiles - tail;
+  }
+  p.num_units = p.n_full + 2 * (p.num_tiles - p.n_full);
   switch (variant) {
     case V1_256: return dispatch_epi<256, 4, false>(epilogue, ta, tb, to, pm, p, s);
     case V1_128: return dispatch_epi<128, 6, false>(epilogue, ta, tb, to, pm, p, s);

@@ -181,7 +181,7 @@ def qk_norm_rope(src, heads, head_dim, q_w, k_w, eps, cos=None, sin=None, rope_r
 def attention_workspace_bytes(seq_q, seq_kv, heads, head_dim, splits=None):
     """Workspace the split-KV path needs (0 when one pass is best)."""
     if splits is None:
-        splits = _native.query("aqb_attention_splits", seq_q, seq_kv, heads, head_dim)
+        return int(_native.query("aqb_attention_auto_workspace_bytes", seq_q, seq_kv, heads, head_dim))
     return int(_native.query("aqb_attention_workspace_bytes", seq_q, heads, head_dim, splits))
 
 

@@ -62,14 +62,51 @@ class Ulysses:
         if video_tokens % self.P:
             raise ConfigError(f"video tokens {video_tokens} not divisible by {self.P} ranks", "parallel.ulysses")
 
+    def _host_staged(self, t: torch.Tensor) -> bool:
+        # gloo (the oversubscribed correctness mode) only reduces/gathers host tensors
+        return t.is_cuda and dist.get_backend(self.group) == "gloo"
+
     def all_to_all(self, out: torch.Tensor, inp: torch.Tensor):
+        if self._host_staged(out):
+            o = out.cpu()
+            dist.all_to_all_single(o, inp.cpu(), group=self.group)
+            out.copy_(o)
+            return
         dist.all_to_all_single(out, inp, group=self.group)
 
     def all_gather(self, out: torch.Tensor, inp: torch.Tensor):
+        if self._host_staged(out):
+            parts = [torch.empty_like(inp, device="cpu") for _ in range(self.P)]
+            dist.all_gather(parts, inp.cpu(), group=self.group)
+            out.copy_(torch.cat(parts).view_as(out))
+            return
         dist.all_gather_into_tensor(out, inp, group=self.group)
 
     def all_reduce_sum(self, t: torch.Tensor):
+        if self._host_staged(t):
+            h = t.cpu()
+            dist.all_reduce(h, op=dist.ReduceOp.SUM, group=self.group)
+            t.copy_(h)
+            return
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+
+def oversubscribed() -> bool:
+    """``AQB_OVERSUBSCRIBE=1``: more ranks than GPUs (e.g. P=8 on 2 GPUs), a correctness-only mode.
+
+    Ranks share GPUs round-robin and the process group is gloo (NCCL refuses two ranks
+    on one device).  The fused p2p exchange is unchanged — CUDA IPC maps a peer's
+    buffer whether it lives on another GPU or on the same one — so the P-rank data
+    path (head/row partition, scatter maps, barrier, split-KV choice) runs exactly as on
+    P GPUs, only time-sliced."""
+    return os.environ.get("AQB_OVERSUBSCRIBE", "0") == "1"
+
+
+def local_device_index() -> int:
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if oversubscribed() and torch.cuda.is_available():
+        return local % torch.cuda.device_count()
+    return local
 
 
 def init_from_env(backend: str | None = None):
@@ -80,8 +117,10 @@ def init_from_env(backend: str | None = None):
     os.environ.setdefault("MASTER_PORT", "29531")
     if backend is None:
         backend = "nccl" if torch.cuda.is_available() else "gloo"
-    if backend == "nccl":
-        torch.cuda.set_device(int(os.environ.get("LOCAL_RANK", "0")))
+    if oversubscribed():
+        backend = "gloo"
+    if torch.cuda.is_available():
+        torch.cuda.set_device(local_device_index())
     dist.init_process_group(backend=backend)
 
 

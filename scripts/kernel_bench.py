@@ -68,7 +68,8 @@ def attn_case(sq, skv, heads, d=128, ncu=False, packed=True):
     qkv = torch.randn(max(sq, skv), 3 * heads * d, device=dev).to(torch.bfloat16)
     o = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
     H = heads * d
-    fn = lambda: ops.attention(qkv[:sq], qkv[:skv, H:], qkv[:skv, 2 * H:], o, heads, d)  # noqa: E731
+    ws = torch.empty(max(16, ops.attention_workspace_bytes(sq, skv, heads, d)), device=dev, dtype=torch.uint8)
+    fn = lambda: ops.attention(qkv[:sq], qkv[:skv, H:], qkv[:skv, 2 * H:], o, heads, d, workspace=ws)  # noqa: E731
     if ncu:
         fn()
         return None
@@ -112,11 +113,14 @@ def main():
     args = ap.parse_args()
     res = []
     S, H = 7800, 2048
-    if args.only in ("all", "gemm", "gemm-proj", "gemm-small"):
+    if args.only in ("all", "gemm", "gemm-proj", "gemm-small", "gemm-n2048"):
         shapes = [(S, 3 * H, H, "bf16"), (S, H, H, "gate_res"), (S, 4 * H, H, "gelu"), (S, H, 4 * H, "gate_res"),
                   (14850 + 256, 3 * 3072, 3072, "bf16"), (8192, 8192, 8192, "bf16")]
         if args.only == "gemm-proj":
             shapes = [(S, H, H, "bf16"), (S, H, H, "f32"), (S, H, H, "gate_res")]
+        if args.only == "gemm-n2048":  # the H-wide projections of a config-2 block (out, cross-q/out, FFN2)
+            shapes = [(S, H, H, "bf16"), (S, H, H, "f32"), (S, H, H, "gate_res"), (S, H, 4 * H, "bf16"),
+                      (S, H, 4 * H, "gate_res")]
         if args.only == "gemm-small":  # one rank's shard at 4 / 8 GPUs (config 2)
             shapes = [(m, n, k, e) for m in (S // 4, S // 8)
                       for (n, k, e) in ((3 * H, H, "bf16"), (H, H, "gate_res"), (4 * H, H, "gelu"), (H, 4 * H, "gate_res"))]

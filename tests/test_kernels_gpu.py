@@ -23,7 +23,9 @@ def rel_l2(a, b):
 
 
 @pytest.mark.parametrize("m,n,k", [(128, 256, 64), (7800, 2048, 2048), (300, 384, 200), (33, 32, 32),
-                                   (1000, 6144, 2048), (257, 128, 4096)])
+                                   (1000, 6144, 2048), (257, 128, 4096),
+                                   # half-width tail units (pair kernel) in the last partial wave
+                                   (7800, 6144, 2048), (1950, 8192, 2048), (1000, 6144, 512)])
 def test_gemm_bf16_matches_fp32(m, n, k):
     g = torch.Generator(device=dev).manual_seed(m + n + k)
     a = torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16)
@@ -264,7 +266,7 @@ def _qkv_ref(a, w, b, qw, kw, heads, rope_rows, cos, sin, row0=0):
     return torch.stack([q, k, x[:, 2]], dim=1)  # [rows, 3, heads, 128]
 
 
-@pytest.mark.parametrize("rows,heads", [(300, 2), (1000, 4), (7800, 16)])
+@pytest.mark.parametrize("rows,heads", [(300, 2), (1000, 4), (7800, 16), (1000, 16)])
 def test_gemm_qknorm_rope_natural_layout(rows, heads):
     g = torch.Generator(device=dev).manual_seed(rows)
     H = heads * 128
@@ -338,7 +340,8 @@ def test_gemm_qknorm_rope_scatter_equals_pack():
 
 @pytest.mark.parametrize("sq,skv,heads,d,splits", [(7800 // 8 * 8 + 256, 8056, 2, 128, 0), (1000, 3000, 2, 128, 3),
                                                    (300, 1000, 3, 128, 5), (200, 600, 4, 64, 2),
-                                                   (96, 400, 4, 32, 4), (257, 129, 1, 128, 2)])
+                                                   (96, 400, 4, 32, 4), (257, 129, 1, 128, 2),
+                                                   (7800, 7800, 16, 128, 0), (25696, 25696, 6, 128, 0)])
 def test_attention_split_kv(sq, skv, heads, d, splits):
     """Split-KV partials + combine equal the single-pass kernel (within bf16 rounding)."""
     g = torch.Generator(device=dev).manual_seed(sq + skv + splits)
@@ -347,8 +350,7 @@ def test_attention_split_kv(sq, skv, heads, d, splits):
     v = torch.randn(skv, heads * d, device=dev, generator=g).to(torch.bfloat16)
     o1 = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
     ops.attention(q, k, v, o1, heads, d, splits=1)
-    ns = splits or _native_splits(sq, skv, heads, d)
-    ws = torch.empty(ops.attention_workspace_bytes(sq, skv, heads, d, ns), device=dev, dtype=torch.uint8)
+    ws = torch.empty(ops.attention_workspace_bytes(sq, skv, heads, d, splits or None), device=dev, dtype=torch.uint8)
     o2 = torch.empty_like(o1)
     ops.attention(q, k, v, o2, heads, d, splits=splits, workspace=ws)
     exp = _attn_ref(q.view(sq, heads, d), k.view(skv, heads, d), v.view(skv, heads, d))
@@ -368,8 +370,18 @@ def test_attention_auto_splits_for_few_heads():
     assert _native_splits(7800, 256, 16, 128) == 1
 
 
+def test_attention_tail_plan():
+    """Config 2 (16 heads x 31 blocks of 256 queries = 496 tiles on 148 SMs): three whole waves,
+    the 52-tile tail split over KV so the last wave is not a third full."""
+    from paper_2505_10584_b200 import _native
+    assert _native.query("aqb_attention_whole_tiles", 7800, 7800, 16, 128) == 3 * 148
+    assert _native_splits(7800, 7800, 16, 128) == 2
+    assert _native.query("aqb_attention_whole_tiles", 7800, 7800, 8, 128) == 248  # no split pays
+    assert ops.attention_workspace_bytes(7800, 7800, 8, 128) == 0
+
+
 @pytest.mark.parametrize("splits,P,rpr,St,hl", [(1, 4, 300, 40, 2), (3, 4, 300, 40, 2), (1, 2, 192, 0, 4),
-                                                (1, 2, 256, 24, 4)])
+                                                (1, 2, 256, 24, 4), (0, 2, 3900, 0, 16), (0, 4, 1950, 256, 16)])
 def test_attention_scatter_rows_to_owners(splits, P, rpr, St, hl):
     """Scatter epilogue: video row r -> rank r // rpr, text rows -> every rank (local stand-ins for peers).
     (2, 192, 0): the last CTA's second Q tile lies wholly past the sequence end (regression)."""
@@ -380,14 +392,14 @@ def test_attention_scatter_rows_to_owners(splits, P, rpr, St, hl):
     qkv = torch.randn(sq, 3, hl, d, device=dev, generator=g).to(torch.bfloat16)
     flat = qkv.view(sq, -1)
     ref_o = torch.empty(sq, hl * d, device=dev, dtype=torch.bfloat16)
+    wsb = ops.attention_workspace_bytes(sq, sq, hl, d, splits or None)
     ops.attention(flat, flat[:, hl * d:], flat[:, 2 * hl * d:], ref_o, hl, d, splits=splits,
-                  workspace=torch.empty(ops.attention_workspace_bytes(sq, sq, hl, d, splits), device=dev,
-                                        dtype=torch.uint8))
+                  workspace=torch.empty(wsb, device=dev, dtype=torch.uint8))
     outs = [torch.zeros(rpr + St, H, device=dev, dtype=torch.bfloat16) for _ in range(P)]
     rank = 1
     dst = [o.data_ptr() + rank * hl * d * 2 for o in outs]
     torch.cuda.synchronize()
-    ws = torch.empty(ops.attention_workspace_bytes(sq, sq, hl, d, splits), device=dev, dtype=torch.uint8)
+    ws = torch.empty(wsb, device=dev, dtype=torch.uint8)
     ops.attention_scatter(flat, flat[:, hl * d:], flat[:, 2 * hl * d:], dst, H, hl, d, rpr, P * rpr, splits=splits,
                           workspace=ws)
     cols = slice(rank * hl * d, (rank + 1) * hl * d)

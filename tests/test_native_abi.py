@@ -68,8 +68,16 @@ def test_attention_split_planner_and_workspace_without_gpu(lib_path):
     assert lib.aqb_attention_splits(8056, 8056, 2, 128) >= 2       # 2 heads x 32 tiles << 148 SMs
     assert lib.aqb_attention_splits(119056, 119056, 24, 128) == 1  # 10k CTAs: no split
     assert lib.aqb_attention_workspace_bytes(1000, 4, 128, 1) == 0
-    rows = 3 * 4 * 1000
+    rows = 3 * (4 * 4) * 256  # splits x (heads x 256-query tiles) x 256 rows, compact partial layout
     assert lib.aqb_attention_workspace_bytes(1000, 4, 128, 3) == ((rows + 63) // 64 * 64 + rows * 128) * 4
+    # wave-quantisation tail (config 2: 16 heads x 31 tiles = 496 on 148 SMs): 3 whole waves + split tail
+    assert lib.aqb_attention_whole_tiles(7800, 7800, 16, 128) == 444
+    assert lib.aqb_attention_splits(7800, 7800, 16, 128) == 2
+    tail_rows = (496 - 444) * 2 * 256
+    assert lib.aqb_attention_auto_workspace_bytes(7800, 7800, 16, 128) == ((tail_rows + 63) // 64 * 64 +
+                                                                          tail_rows * 128) * 4
+    assert lib.aqb_attention_whole_tiles(7800, 7800, 8, 128) == 248  # 248 tiles: splitting never pays
+    assert lib.aqb_attention_auto_workspace_bytes(7800, 7800, 8, 128) == 0
 
 
 def test_peer_barrier_validates_before_launch(lib_path):
