@@ -39,6 +39,11 @@ namespace gemm {
 constexpr int BM = 128;
 constexpr int BK = 64;  // 64 bf16 = 128 B rows -> SWIZZLE_128B
 constexpr int kThreads = 256;
+// Internal epilogue (not in the C-ABI): AQB_EPI_GATE_RES without the bf16 copy.  The
+// epilogue stages gate * (acc + bias) and a TMA reduce-add performs residual += it at
+// L2, so the SM never reads the residual: no residual buffers (full pipeline depth)
+// and a third of the epilogue's shared-memory traffic.
+constexpr int kEpiGateAdd = 100;
 constexpr int kEpiBuf = 128 * 128;  // one epilogue chunk: 128 rows x 128 B
 constexpr int kAuxBuf = 128 * 64;   // bf16 copy of a gate*residual chunk: 128 rows x 64 B (64B swizzle)
 
@@ -186,7 +191,7 @@ template <int EPI>
 constexpr int aux_bytes() { return EPI == AQB_EPI_GATE_RES ? 2 * kAuxBuf : 0; }
 
 template <int EPI>
-constexpr int epi_cols() { return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES) ? 32 : 64; }
+constexpr int epi_cols() { return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES || EPI == kEpiGateAdd) ? 32 : 64; }
 
 // Request residual chunk `idx` (leader thread; no-op past the last tile / column N).
 template <int BN, int NB>
@@ -405,6 +410,14 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
         for (int i = 0; i < 8; ++i)
           st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(v[4 * i]), __float_as_uint(v[4 * i + 1]),
                        __float_as_uint(v[4 * i + 2]), __float_as_uint(v[4 * i + 3]));
+      } else if constexpr (EPI == kEpiGateAdd) {
+        const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float4 g = (p.gate && col0 + 4 * i < p.N) ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+          st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(g.x * v[4 * i]), __float_as_uint(g.y * v[4 * i + 1]),
+                       __float_as_uint(g.z * v[4 * i + 2]), __float_as_uint(g.w * v[4 * i + 3]));
+        }
       } else {
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -418,7 +431,10 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       fence_proxy_async_smem();
       named_bar_sync(1, 128);
       if (leader_thread) {
-        tma_store_2d(tmo, buf, col0, row0);  // clips rows >= M and columns >= N
+        if constexpr (EPI == kEpiGateAdd)
+          tma_reduce_add_2d(tmo, buf, col0, row0);  // residual += staged tile (clipped like a store)
+        else
+          tma_store_2d(tmo, buf, col0, row0);  // clips rows >= M and columns >= N
         if constexpr (EPI == AQB_EPI_GATE_RES) {
           if (p.aux != nullptr) tma_store_2d(&pm->m[0], abuf, col0, row0);
         }
@@ -733,6 +749,7 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
     case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_GATE_RES: return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32, PAIR>(ta, tb, to, pm, p, s);
+    case kEpiGateAdd: return launch<BN, STAGES, kEpiGateAdd, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_QKNORM_ROPE: return launch<BN, STAGES, AQB_EPI_QKNORM_ROPE, PAIR>(ta, tb, to, pm, p, s);
   }
@@ -744,6 +761,16 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
 // bytes each SM loads.  AQB_GEMM_VARIANT=1cta256|1cta128|2cta256|2cta128
 // forces one (benchmarking).
 enum Variant { V1_256 = 0, V1_128, V2_256, V2_128 };
+
+// AQB_GEMM_GATE_ADD=0: gate*residual always through the residual-reading epilogue (benchmarking)
+static bool gate_add_enabled() {
+  static int enabled = -1;
+  if (enabled < 0) {
+    const char* e = getenv("AQB_GEMM_GATE_ADD");
+    enabled = (e && !strcmp(e, "0")) ? 0 : 1;
+  }
+  return enabled == 1;
+}
 
 // Tiles of a pair-kernel launch (BN = 256) that run as two half-width units: the
 // partial last wave when it fills at most half the CTA pairs (it then takes half a
@@ -902,6 +929,7 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
     if (rc) return rc;
     return run(a, lda, w, ldw, m, n, k, epilogue, p, to, variant, reinterpret_cast<cudaStream_t>(stream), &xm);
   }
+  if (epilogue == AQB_EPI_GATE_RES && gate_add_enabled()) epilogue = kEpiGateAdd;
   return run(a, lda, w, ldw, m, n, k, epilogue, p, to, variant, reinterpret_cast<cudaStream_t>(stream));
 }
 

@@ -305,6 +305,13 @@ AQB_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int32_t x, int3
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+// out[tile] += smem tile (f32 add performed at L2; no read of `out` by the SM)
+AQB_DEV void tma_reduce_add_2d(const CUtensorMap* m, const void* src, int32_t x, int32_t y) {
+  asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(smem_u32(src)), "r"(x), "r"(y)
+               : "memory");
+}
 AQB_DEV void tma_store_3d(const CUtensorMap* m, const void* src, int32_t c0, int32_t c1, int32_t c2) {
   asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
                    reinterpret_cast<uint64_t>(m)),
