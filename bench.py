@@ -171,7 +171,7 @@ def run_reference(args):
         "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_s": wall,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     return 0
 
 
@@ -236,7 +236,7 @@ def mmdit_720p(sp, timed, rank):
 def run_ours(args):
     from paper_2505_10584_b200 import SINGLE_DIT_2B, build_model, denoise, no_cache, plan_cache, flops_per_step
     from paper_2505_10584_b200 import ops
-    from paper_2505_10584_b200.parallel import Ulysses, init_from_env, local_device_index
+    from paper_2505_10584_b200.parallel import TensorSP, Ulysses, init_from_env, local_device_index
     from paper_2505_10584_b200.sampler import _Graphs
     from paper_2505_10584_b200.weights import init_weights, synthetic_inputs
     import torch.distributed as dist
@@ -246,7 +246,7 @@ def run_ours(args):
     sp = None
     if world > 1:
         init_from_env("nccl")
-        sp = Ulysses()
+        sp = TensorSP() if args.parallel == "tp" else Ulysses()
     torch.cuda.set_device(local)
     rank = sp.rank if sp else 0
     cfg = SINGLE_DIT_2B
@@ -367,7 +367,7 @@ def run_ours(args):
         _log(rank, "mmdit 720p")
         del model, graphs
         torch.cuda.empty_cache()
-        mm = mmdit_720p(sp, timed, rank)
+        mm = mmdit_720p(Ulysses() if (sp and sp.tensor_parallel) else sp, timed, rank)
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -376,8 +376,12 @@ def run_ours(args):
             "config": {"workload": "config2: Single-DiT-2B (fitted H=2048 A=16 L=28), 17x480x832 -> 7,800 tokens, "
                                    "text 256x4096, 30 Euler steps, cache on = plan_cache(30) (17 full/13 cached); "
                                    "1 bench step = 1 video",
-                       "parallelism": f"ulysses-sp{world}" if world > 1 else "single-gpu",
-                       "ulysses_exchange": (sp.exchange + (" (QKV-GEMM and attention epilogues store into peer "
+                       "parallelism": (f"tp{world}-sp" if args.parallel == "tp" else f"ulysses-sp{world}")
+                       if world > 1 else "single-gpu",
+                       "tp_exchange": ("p2p: all-gather stored by the LN+modulate kernel into every rank, "
+                                       "reduce-scatter as TMA reduce-add from the row-parallel GEMM epilogues; "
+                                       "device barrier") if (sp and sp.tensor_parallel) else None,
+                       "ulysses_exchange": None if (sp and sp.tensor_parallel) else (sp.exchange + (" (QKV-GEMM and attention epilogues store into peer "
                                             "memory over NVLink; device barrier)" if sp.exchange == "p2p" else
                                             " all_to_all")) if sp else None,
                        "l2": "inputs larger than L2 (4.3 GB of bf16 weights streamed per step)",
@@ -401,7 +405,7 @@ def run_ours(args):
             c = cpu_reference_sample(threads)
             line["cpu_baseline"] = {"value": c["steps_per_s_cache_on"], "unit": UNIT, "cores": threads, "kind": "port",
                                     "sample": c["sample"]}
-        print(json.dumps(line), flush=True)
+        emit(line)
     _log(rank, "done")
     if sp:
         dist.barrier()
@@ -413,7 +417,22 @@ def run_ours(args):
     os._exit(0)
 
 
+_JSON_OUT = None
+
+
+def emit(line: dict):
+    """The one JSON line on the real stdout (library chatter, e.g. NCCL's version banner, goes to stderr)."""
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def main():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)  # fd 1 (C and Python prints) -> stderr for the rest of the run
+    sys.stdout = sys.stderr
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3)
@@ -422,6 +441,9 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-mmdit", action="store_true", help="skip the 13.4B MM-DiT 720p companion measurement")
+    ap.add_argument("--parallel", choices=["ulysses", "tp"], default="ulysses",
+                    help="N>1: Ulysses sequence parallel (default) or TP-SP (Single-DiT; the MM-DiT companion "
+                         "then runs Ulysses)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

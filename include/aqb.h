@@ -57,6 +57,25 @@ int aqb_sm_count(void);
 int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* y, int64_t ldy,
                       int64_t rows, int32_t hidden, float eps, int32_t norm_kind, float* probe_prev,
                       float* probe_partials, const int32_t* run_flag, int32_t run_if, void* stream);
+/* TP-SP "AllGather + ..." (sequence-parallel LayerNorm feeding a
+ * column-parallel projection): as aqb_norm_modulate, but row i is stored into each
+ * of the ny (1..8) outputs y[d] + i*ldy — every rank's gathered buffer, at this
+ * rank's row offset (peer memory over NVLink), so the all-gather is the kernel's
+ * own stores.  16-byte aligned outputs. */
+/* TP-SP "Out_Linear / FFN_Linear2 + ReduceScatter" fused: this
+ * rank's partial of a row-parallel projection, gate[n] * (acc + bias) (bias NULL on all
+ * but one rank), is reduce-added (f32, at the destination) into the residual of the
+ * rank owning each row: row i -> peer_out[i / rows_per_rank] + (i % rows_per_rank)*ldo.
+ * m == nranks * rows_per_rank.  Summation order across ranks is not fixed (f32
+ * reductions race at the owner), so results are not bitwise reproducible run to run. */
+int aqb_gemm_gate_add_scatter(const void* a, int64_t lda, const void* w, int64_t ldw, float* const* peer_out,
+                              int32_t nranks, int64_t ldo, int64_t rows_per_rank, int64_t m, int64_t n, int64_t k,
+                              const float* bias, const float* gate, const int32_t* run_flag, int32_t run_if,
+                              void* stream);
+int aqb_norm_modulate_gather(const float* x, int64_t ldx, const float* shift, const float* scale, void* const* y,
+                             int32_t ny, int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
+                             float* probe_prev, float* probe_partials, const int32_t* run_flag, int32_t run_if,
+                             void* stream);
 
 /* ---------------------------------------------------------------------------
  * Projection GEMMs (AllGather+QKV_Linear, Out_Linear, FFN_Linear1/2, GeLU and

@@ -10,7 +10,8 @@ Public API (drop-in for the reference's cache-schedule boundary,
   ``WindowPlan`` (``inference.py:89-279``), with GPU blend / Eq. 3 kernels
 * new: ``RelL1Policy``, ``DiTConfig`` + presets, ``SingleDiT`` / ``MMDiT``
   (model construction), ``denoise`` (sampler loop), ``denoise_windows``
-  (temporal MultiDiffusion), ``latent_shape``, ``token_count``.
+  (temporal MultiDiffusion), ``latent_shape``, ``token_count``; multi-GPU
+  groups ``Ulysses`` (sequence parallel) and ``TensorSP`` (TP-SP, Single-DiT).
 
 The model/sampler symbols need CUDA and ``libaqb.so`` (hand-written sm_100a
 kernels); they are imported lazily so the schedule API works anywhere.
@@ -53,6 +54,9 @@ _LAZY = {
     "denoise": ("sampler", "denoise"),
     "DenoiseResult": ("sampler", "DenoiseResult"),
     "denoise_windows": ("sampler", "denoise_windows"),
+    "SingleDiTTP": ("model", "SingleDiTTP"),
+    "Ulysses": ("parallel", "Ulysses"),
+    "TensorSP": ("parallel", "TensorSP"),
 }
 
 
@@ -70,6 +74,7 @@ __all__ = [
     "DiTConfig", "MM_DIT_13B", "NativeError", "PRESETS", "PlanningError", "RelL1Policy", "SINGLE_DIT_2B",
     "TINY_MM", "TINY_SINGLE", "VaeSpec", "VideoSpec", "composite_speedup", "dit_parallel_latency",
     "flops_per_step", "front_block_count", "latent_shape", "no_cache", "plan_cache", "token_count",
-    "SingleDiT", "MMDiT", "build_model", "denoise", "DenoiseResult", "denoise_windows",
+    "SingleDiT", "MMDiT", "SingleDiTTP", "build_model", "denoise", "DenoiseResult", "denoise_windows",
+    "Ulysses", "TensorSP",
     "Tile", "TilePlan", "WindowPlan", "plan_vae_tiles", "plan_temporal_windows",
 ]

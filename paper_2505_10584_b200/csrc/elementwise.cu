@@ -40,11 +40,22 @@ AQB_DEV void store2(__nv_bfloat16* p, float2 v) {
 }
 AQB_DEV void store2(float* p, float2 v) { *reinterpret_cast<float2*>(p) = v; }
 
+// Output rows go to up to 8 destinations (same row index and stride in each): one
+// for the plain kernel; every rank's gathered buffer for the TP-SP all-gather
+// (aqb_norm_modulate_gather: the rows this rank normalised are stored straight into
+// each peer's copy over NVLink, so no separate all-gather runs).
+constexpr int kMaxOuts = 8;
+template <typename OutT>
+struct Outs {
+  OutT* p[kMaxOuts];
+  int n;
+};
+
 // OutT = bf16 (product path) or float (fp32 validation mode).
 template <int NV, typename OutT>
 __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__ x, int64_t ldx,
                                                        const float* __restrict__ shift,
-                                                       const float* __restrict__ scale, OutT* __restrict__ y,
+                                                       const float* __restrict__ scale, const Outs<OutT> ys,
                                                        int64_t ldy, int64_t rows, float eps, int kind,
                                                        float* __restrict__ prev, float* __restrict__ partials,
                                                        const int32_t* flag, int32_t run_if) {
@@ -78,7 +89,7 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
   }
   const float4* sh4 = reinterpret_cast<const float4*>(shift);
   const float4* sc4 = reinterpret_cast<const float4*>(scale);
-  OutT* yr = y + row * ldy;
+  const int64_t yoff = row * ldy;
   float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
   float dsum = 0.f, psum = 0.f;
 #pragma unroll
@@ -91,7 +102,8 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
     o.y = (v[j].y - mean) * rstd * (1.f + sc.y) + sh.y;
     o.z = (v[j].z - mean) * rstd * (1.f + sc.z) + sh.z;
     o.w = (v[j].w - mean) * rstd * (1.f + sc.w) + sh.w;
-    store4(yr + 4 * c4, o);
+#pragma unroll 1
+    for (int d = 0; d < ys.n; ++d) store4(ys.p[d] + yoff + 4 * c4, o);
     if (pr) {
       const float4 p = pr[c4];
       dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
@@ -128,7 +140,7 @@ AQB_DEV float block_sum(float v, float* red) {
 template <int NW, typename OutT>
 __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __restrict__ x, int64_t ldx,
                                                                const float* __restrict__ shift,
-                                                               const float* __restrict__ scale, OutT* __restrict__ y,
+                                                               const float* __restrict__ scale, const Outs<OutT> ys,
                                                                int64_t ldy, int64_t rows, float eps, int kind,
                                                                float* __restrict__ prev, float* __restrict__ partials,
                                                                const int32_t* flag, int32_t run_if) {
@@ -162,7 +174,7 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
   }
   const float4* sh4 = reinterpret_cast<const float4*>(shift);
   const float4* sc4 = reinterpret_cast<const float4*>(scale);
-  OutT* yr = y + row * ldy;
+  const int64_t yoff = row * ldy;
   float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
   float dsum = 0.f, psum = 0.f;
 #pragma unroll
@@ -175,7 +187,8 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
     o.y = (v[j].y - mean) * rstd * (1.f + sc.y) + sh.y;
     o.z = (v[j].z - mean) * rstd * (1.f + sc.z) + sh.z;
     o.w = (v[j].w - mean) * rstd * (1.f + sc.w) + sh.w;
-    store4(yr + 4 * c4, o);
+#pragma unroll 1
+    for (int d = 0; d < ys.n; ++d) store4(ys.p[d] + yoff + 4 * c4, o);
     if (pr) {
       const float4 p = pr[c4];
       dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
@@ -465,10 +478,17 @@ static int grid_for(int64_t n, int threads) {
 using namespace aqb;
 
 template <typename OutT>
-static int norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* y, int64_t ldy,
-                         int64_t rows, int32_t hidden, float eps, int32_t norm_kind, float* probe_prev,
-                         float* probe_partials, const int32_t* run_flag, int32_t run_if, void* stream) {
-  AQB_CHECK_ARG(x && y, "norm_modulate: null pointer");
+static int norm_modulate(const float* x, int64_t ldx, const float* shift, const float* scale, void* const* y,
+                         int32_t ny, int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
+                         float* probe_prev, float* probe_partials, const int32_t* run_flag, int32_t run_if,
+                         void* stream) {
+  AQB_CHECK_ARG(x && y && ny >= 1 && ny <= kMaxOuts, "norm_modulate: null pointer or 1..%d outputs", kMaxOuts);
+  Outs<OutT> yb{};
+  yb.n = ny;
+  for (int d = 0; d < ny; ++d) {
+    AQB_CHECK_ARG(y[d] && reinterpret_cast<uintptr_t>(y[d]) % 16 == 0, "norm_modulate: output %d null/misaligned", d);
+    yb.p[d] = reinterpret_cast<OutT*>(y[d]);
+  }
   AQB_CHECK_ARG(hidden % 128 == 0 && hidden >= 128 && hidden <= 4096, "norm_modulate: hidden %d unsupported", hidden);
   AQB_CHECK_ARG(ldx % 4 == 0 && ldy % 4 == 0 && ldx >= hidden && ldy >= hidden, "norm_modulate: bad strides");
   AQB_CHECK_ARG(!probe_prev || probe_partials, "norm_modulate: probe needs partials");
@@ -476,7 +496,6 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
   if (rows <= 0) return AQB_OK;
   const int grid = static_cast<int>((rows + 7) / 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  OutT* yb = reinterpret_cast<OutT*>(y);
   if (hidden >= 1024 && hidden % 512 == 0) {  // CTA per row (hidden/16 threads)
     switch (hidden / 512) {
 #define NMR_CASE(NW)                                                                                               \
@@ -511,7 +530,16 @@ extern "C" int aqb_norm_modulate(const float* x, int64_t ldx, const float* shift
                                  int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
                                  float* probe_prev, float* probe_partials, const int32_t* run_flag, int32_t run_if,
                                  void* stream) {
-  return norm_modulate<__nv_bfloat16>(x, ldx, shift, scale, y, ldy, rows, hidden, eps, norm_kind, probe_prev,
+  void* ys[1] = {y};
+  return norm_modulate<__nv_bfloat16>(x, ldx, shift, scale, ys, 1, ldy, rows, hidden, eps, norm_kind, probe_prev,
+                                      probe_partials, run_flag, run_if, stream);
+}
+
+extern "C" int aqb_norm_modulate_gather(const float* x, int64_t ldx, const float* shift, const float* scale,
+                                        void* const* y, int32_t ny, int64_t ldy, int64_t rows, int32_t hidden,
+                                        float eps, int32_t norm_kind, float* probe_prev, float* probe_partials,
+                                        const int32_t* run_flag, int32_t run_if, void* stream) {
+  return norm_modulate<__nv_bfloat16>(x, ldx, shift, scale, y, ny, ldy, rows, hidden, eps, norm_kind, probe_prev,
                                       probe_partials, run_flag, run_if, stream);
 }
 
@@ -519,7 +547,8 @@ extern "C" int aqb_norm_modulate_f32(const float* x, int64_t ldx, const float* s
                                      int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
                                      float* probe_prev, float* probe_partials, const int32_t* run_flag,
                                      int32_t run_if, void* stream) {
-  return norm_modulate<float>(x, ldx, shift, scale, y, ldy, rows, hidden, eps, norm_kind, probe_prev,
+  void* ys[1] = {y};
+  return norm_modulate<float>(x, ldx, shift, scale, ys, 1, ldy, rows, hidden, eps, norm_kind, probe_prev,
                               probe_partials, run_flag, run_if, stream);
 }
 

@@ -44,6 +44,12 @@ constexpr int kThreads = 256;
 // L2, so the SM never reads the residual: no residual buffers (full pipeline depth)
 // and a third of the epilogue's shared-memory traffic.
 constexpr int kEpiGateAdd = 100;
+// Internal epilogue of aqb_gemm_gate_add_scatter (TP-SP row-parallel projection +
+// reduce-scatter): the same staged gate * (acc + bias), reduce-added into the residual
+// of the rank that owns each row (peer memory) — a TMA reduce-add per 128-row CTA
+// block that lies in one rank's rows, per-thread red.global.add.v4 for a block that
+// straddles two ranks.
+constexpr int kEpiGateAddScatter = 101;
 constexpr int kEpiBuf = 128 * 128;  // one epilogue chunk: 128 rows x 128 B
 constexpr int kAuxBuf = 128 * 64;   // bf16 copy of a gate*residual chunk: 128 rows x 64 B (64B swizzle)
 
@@ -73,6 +79,9 @@ struct Params {
   int hpg, g_base, groups;  // heads per output group (Ulysses), group offset, group count
   int peer_groups;          // 1: group g is TMA-stored through PeerMaps::m[g] (another rank's buffer)
   float eps;
+  // gate-add scatter (kEpiGateAddScatter): rank r's residual, rows_per_rank rows of stride ldo
+  float* red_dst[8];
+  int64_t red_rpr;
 };
 
 // Per-destination-rank output maps of the Ulysses scatter (QK-norm epilogue):
@@ -191,7 +200,9 @@ template <int EPI>
 constexpr int aux_bytes() { return EPI == AQB_EPI_GATE_RES ? 2 * kAuxBuf : 0; }
 
 template <int EPI>
-constexpr int epi_cols() { return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES || EPI == kEpiGateAdd) ? 32 : 64; }
+constexpr int epi_cols() {
+  return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES || EPI == kEpiGateAdd || EPI == kEpiGateAddScatter) ? 32 : 64;
+}
 
 // Request residual chunk `idx` (leader thread; no-op past the last tile / column N).
 template <int BN, int NB>
@@ -410,6 +421,34 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
         for (int i = 0; i < 8; ++i)
           st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(v[4 * i]), __float_as_uint(v[4 * i + 1]),
                        __float_as_uint(v[4 * i + 2]), __float_as_uint(v[4 * i + 3]));
+      } else if constexpr (EPI == kEpiGateAddScatter) {
+        const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
+        const int64_t first = int64_t(row0), last = min(int64_t(row0) + BM, int64_t(p.M)) - 1;
+        if (first / p.red_rpr == last / p.red_rpr) {  // CTA block inside one rank: stage for TMA
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const float4 g = (p.gate && col0 + 4 * i < p.N) ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+            st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(g.x * v[4 * i]),
+                         __float_as_uint(g.y * v[4 * i + 1]), __float_as_uint(g.z * v[4 * i + 2]),
+                         __float_as_uint(g.w * v[4 * i + 3]));
+          }
+        } else {  // straddles a rank boundary: each thread reduces its own row
+          const int64_t row = int64_t(row0) + r;
+          if (row < p.M) {
+            const int64_t rk = row / p.red_rpr;
+            float* dst = p.red_dst[rk] + (row - rk * p.red_rpr) * p.ldo + col0;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) {
+              if (col0 + 4 * i < p.N) {
+                const float4 g = p.gate ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+                red_add_v4_sys(dst + 4 * i, g.x * v[4 * i], g.y * v[4 * i + 1], g.z * v[4 * i + 2],
+                               g.w * v[4 * i + 3]);
+              }
+            }
+          }
+          ++es.chunk;
+          continue;  // uniform: no staged tile, no TMA op for this chunk
+        }
       } else if constexpr (EPI == kEpiGateAdd) {
         const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
 #pragma unroll
@@ -433,6 +472,8 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       if (leader_thread) {
         if constexpr (EPI == kEpiGateAdd)
           tma_reduce_add_2d(tmo, buf, col0, row0);  // residual += staged tile (clipped like a store)
+        else if constexpr (EPI == kEpiGateAddScatter)
+          tma_reduce_add_2d(&pm->m[row0 / p.red_rpr], buf, col0, int(row0 % p.red_rpr));  // owner's rows
         else
           tma_store_2d(tmo, buf, col0, row0);  // clips rows >= M and columns >= N
         if constexpr (EPI == AQB_EPI_GATE_RES) {
@@ -750,6 +791,7 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
     case AQB_EPI_GATE_RES: return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32, PAIR>(ta, tb, to, pm, p, s);
     case kEpiGateAdd: return launch<BN, STAGES, kEpiGateAdd, PAIR>(ta, tb, to, pm, p, s);
+    case kEpiGateAddScatter: return launch<BN, STAGES, kEpiGateAddScatter, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_QKNORM_ROPE: return launch<BN, STAGES, AQB_EPI_QKNORM_ROPE, PAIR>(ta, tb, to, pm, p, s);
   }
@@ -791,7 +833,7 @@ static int half_tail_tiles(int tiles, bool pair, int bn) {
   return (tiles > pairs && r > 0 && 2 * r <= pairs) ? r : 0;
 }
 
-static int pick_variant(int64_t m, int64_t n, int64_t k) {
+static int pick_variant(int64_t m, int64_t n, int64_t k, bool f32_out = false) {
   static int forced = -2;
   if (forced == -2) {
     forced = -1;
@@ -818,6 +860,14 @@ static int pick_variant(int64_t m, int64_t n, int64_t k) {
     const double l2 = bytes / 64.0;                           // ~64 B/cycle/SM sustainable from L2
     const double t = waves * std::max(mma, l2) * double(k);
     if (t < best * 0.97) best = t, bv = c.v;
+  }
+  // f32-output epilogues (gate*residual, reduce-scatter) on a shard small enough that the
+  // 256x256 pair tiles fill at most one wave: nothing overlaps the exposed f32 epilogue,
+  // and 256x128 pair tiles (twice the CTAs, half the epilogue each) measured faster:
+  // 1950x2048x2048 515 -> 592 TFLOP/s, 975x2048x8192 561 -> 821.
+  if (f32_out && bv == V2_256) {
+    const double tiles = double((m + 255) / 256) * double((n + 255) / 256);
+    if (tiles <= sms / 2) bv = V2_128;
   }
   return bv;
 }
@@ -898,7 +948,7 @@ extern "C" int aqb_gemm_bf16(const void* a, int64_t lda, const void* w, int64_t 
   AQB_CHECK_ARG(ldo >= n && ldo % 8 == 0, "gemm: bad ldo");
   AQB_CHECK_ARG(m < (1ll << 31) && n < (1ll << 31), "gemm: shape too large");
 
-  const int variant = pick_variant(m, n, k);
+  const int variant = pick_variant(m, n, k, epilogue == AQB_EPI_GATE_RES || epilogue == AQB_EPI_F32);
   CUtensorMap to;
   if (epilogue == AQB_EPI_EULER) {
     memset(&to, 0, sizeof(to));  // direct stores; map unused
@@ -1010,4 +1060,37 @@ extern "C" int aqb_gemm_qknorm_rope_scatter(const void* a, int64_t lda, const vo
   return aqb::gemm::qknorm_rope(a, lda, w, ldw, m, n, k, bias, part_width, norm_parts, q_w, k_w, eps, rope_cos,
                                 rope_sin, rope_row0, rope_rows, nullptr, out_row_stride, nranks, 0, hpg, 0, peer_out,
                                 run_flag, run_if, reinterpret_cast<cudaStream_t>(stream));
+}
+
+extern "C" int aqb_gemm_gate_add_scatter(const void* a, int64_t lda, const void* w, int64_t ldw, float* const* peer_out,
+                                         int32_t nranks, int64_t ldo, int64_t rows_per_rank, int64_t m, int64_t n,
+                                         int64_t k, const float* bias, const float* gate, const int32_t* run_flag,
+                                         int32_t run_if, void* stream) {
+  using namespace aqb;
+  using namespace aqb::gemm;
+  AQB_CHECK_ARG(a && w && peer_out, "gemm_gate_add_scatter: null pointer");
+  AQB_CHECK_ARG(nranks >= 1 && nranks <= kMaxPeers, "gemm_gate_add_scatter: 1..%d ranks", kMaxPeers);
+  AQB_CHECK_ARG(m >= 1 && n >= 1 && k >= 1 && k % 8 == 0 && n % 16 == 0, "gemm_gate_add_scatter: bad shape");
+  AQB_CHECK_ARG(lda % 8 == 0 && ldw % 8 == 0 && lda >= k && ldw >= k, "gemm_gate_add_scatter: bad lda/ldw");
+  AQB_CHECK_ARG(ldo >= n && ldo % 4 == 0, "gemm_gate_add_scatter: bad ldo");
+  AQB_CHECK_ARG(rows_per_rank >= 1 && rows_per_rank * nranks == m, "gemm_gate_add_scatter: m != nranks * rows_per_rank");
+  Params p{};
+  p.out = peer_out[0], p.ldo = ldo, p.bias = bias, p.gate = gate;
+  p.run_flag = run_flag, p.run_if = run_if;
+  p.red_rpr = rows_per_rank;
+  PeerMaps pm;
+  memset(&pm, 0, sizeof(pm));
+  for (int r = 0; r < nranks; ++r) {
+    AQB_CHECK_ARG(peer_out[r] && reinterpret_cast<uintptr_t>(peer_out[r]) % 16 == 0,
+                  "gemm_gate_add_scatter: peer_out[%d] null/misaligned", r);
+    p.red_dst[r] = peer_out[r];
+    const uint64_t dims[2] = {uint64_t(n), uint64_t(rows_per_rank)};
+    const uint64_t strides[1] = {uint64_t(ldo) * 4};
+    const uint32_t box[2] = {32, uint32_t(BM)};
+    int rc = make_tmap(&pm.m[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, peer_out[r], 2, dims, strides, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  return run(a, lda, w, ldw, m, n, k, kEpiGateAddScatter, p, pm.m[0], pick_variant(m, n, k, true),
+             reinterpret_cast<cudaStream_t>(stream), &pm);
 }

@@ -305,6 +305,12 @@ AQB_DEV void tma_store_2d(const CUtensorMap* m, const void* src, int32_t x, int3
                "r"(smem_u32(src)), "r"(x), "r"(y)
                : "memory");
 }
+// *p += (a, b, c, d) at the memory's home L2 (system scope: the address may be another
+// GPU's memory that other GPUs reduce into concurrently)
+AQB_DEV void red_add_v4_sys(float* p, float a, float b, float c, float d) {
+  asm volatile("red.relaxed.sys.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(p), "f"(a), "f"(b), "f"(c), "f"(d)
+               : "memory");
+}
 // out[tile] += smem tile (f32 add performed at L2; no read of `out` by the SM)
 AQB_DEV void tma_reduce_add_2d(const CUtensorMap* m, const void* src, int32_t x, int32_t y) {
   asm volatile("cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3}], [%1];" ::"l"(

@@ -37,7 +37,7 @@ import torch
 from . import ops
 from .config import DiTConfig
 from .errors import ConfigError
-from .parallel import SIGNAL_BYTES, PeerBuffers, Ulysses, exchange_offsets
+from .parallel import SIGNAL_BYTES, PeerBuffers, Ulysses, exchange_offsets, tp_shard_single_dit
 from .schedule import front_block_count
 from .weights import init_weights
 
@@ -165,10 +165,12 @@ class DiTModel:
             self.xq = e(Sv_loc, H)
             # step-independent cross-attention K/V of the text, once per call (K RMS-normed)
             self.text_kv = []
+            heads = A // P if self._tp() else A  # TP-SP: this rank's heads
             for i in range(cfg.num_single):
-                kv = e(cfg.text_len, 2 * H)
+                kv = e(cfg.text_len, 2 * heads * D)
                 ops.gemm(t_bf, W[f"blocks.{i}.xkv.w"], kv, bias=W[f"blocks.{i}.xkv.b"])
-                ops.qk_norm_rope(kv, A, D, W[f"blocks.{i}.xk_norm"], None, cfg.qk_norm_eps, parts=2, norm_parts=1)
+                ops.qk_norm_rope(kv, heads, D, W[f"blocks.{i}.xk_norm"], None, cfg.qk_norm_eps, parts=2,
+                                 norm_parts=1)
                 self.text_kv.append(kv)
         else:
             if pooled is None or pooled.shape != (cfg.pooled_dim,):
@@ -187,7 +189,9 @@ class DiTModel:
         self.cache_mode = "dit-layer-cache"
         hl = A // P
         self.hl = hl
-        if self.sp is not None and P > 1:
+        if self._tp():
+            self._prepare_tp()
+        elif self.sp is not None and P > 1:
             if self.sp.exchange == "p2p" and D == 128:
                 # symmetric buffers: attention input (all heads of this rank's group, full
                 # sequence) and the residual-row-major attention output
@@ -212,9 +216,16 @@ class DiTModel:
         # split-KV workspace for the attention launches of this geometry
         need = ops.attention_workspace_bytes(Sv + St if P > 1 else rows, Sv + St, hl, D)
         if cfg.family == "single-dit":
-            need = max(need, ops.attention_workspace_bytes(Sv_loc, cfg.text_len, A, D))
+            xq_rows, xheads = (Sv, hl) if self._tp() else (Sv_loc, A)
+            need = max(need, ops.attention_workspace_bytes(xq_rows, cfg.text_len, xheads, D))
         self.attn_ws = torch.empty(max(need, 16), device=dev, dtype=torch.uint8)
         return self
+
+    def _tp(self) -> bool:
+        return self.sp is not None and getattr(self.sp, "tensor_parallel", False)
+
+    def _prepare_tp(self):
+        raise ConfigError("TP-SP is implemented for Single-DiT", "parallel.tp")
 
     def _barrier(self, flag=None, run_if=1, payload=None):
         ops.peer_barrier(self.sig, self.sp.rank, self.epoch, self.peer_status, payload=payload,
@@ -471,6 +482,8 @@ class DiTModel:
             raise ConfigError("call prepare() first", "model")
         if cache_mode not in ("dit-layer-cache", "attention-cache"):
             raise ConfigError("unknown cache mode", "cache.mode")
+        if cache_mode == "attention-cache" and self._tp():
+            raise ConfigError("attention-cache mode is not implemented under TP-SP", "cache.mode")
         self.cache_mode = cache_mode
         if cache_mode == "attention-cache":
             self._alloc_attention_cache()
@@ -642,5 +655,114 @@ class MMDiT(DiTModel):
         super().__init__(cfg, **kw)
 
 
+class SingleDiTTP(SingleDiT):
+    """Single-DiT under TP-SP (:class:`~paper_2505_10584_b200.parallel.TensorSP`).
+
+    Weights are sharded at construction (:func:`~paper_2505_10584_b200.parallel.tp_shard_single_dit`):
+    QKV / cross-attention q and text K/V / FFN1 by output rows (this rank's A/P heads, F/P
+    hidden columns), the out / cross-out / FFN2 projections by input columns (their bias on
+    rank 0 only).  AdaLN tables, timestep MLP, patch embed and final layer are replicated.
+    Per block, six sub-steps each end in ``aqb_peer_barrier``:
+
+      AG(LN+mod(x))  -> QKV(local heads, all rows) -> attention -> proj  -> RS into x
+      AG(bf16 x)     -> q(local heads) -> cross-attention to text -> proj -> RS into x
+      AG(LN+mod(x))  -> FFN1(local columns, GeLU) -> FFN2 -> RS into x
+
+    The reduce-scatter sums float32 partials at the owning rank in arrival order, so a
+    run is reproducible only to rounding (not bitwise) — unlike the Ulysses path.
+    """
+
+    def __init__(self, cfg: DiTConfig, sp=None, **kw):
+        if sp is None or not getattr(sp, "tensor_parallel", False):
+            raise ConfigError("SingleDiTTP needs a TensorSP group", "parallel.tp")
+        if kw.get("precision", "bf16") != "bf16":
+            raise ConfigError("TP-SP runs the bf16 product path", "model.precision")
+        if cfg.head_dim != 128:
+            raise ConfigError("TP-SP needs head_dim 128 (fused QK-norm epilogue)", "parallel.tp")
+        super().__init__(cfg, sp=sp, **kw)
+        self.W = tp_shard_single_dit(self.W, cfg, sp.P, sp.rank)
+        torch.cuda.empty_cache()
+
+    def _prepare_tp(self):
+        cfg, g, dev = self.cfg, self.geo, self.device
+        H, D, P = cfg.hidden_size, cfg.head_dim, self.sp.P
+        self.sp.check(cfg.num_heads, g.Sv, cfg.ffn_dim)
+        hd = self.hl * D
+        S, n = g.Sv, g.Sv_loc
+        # symmetric buffers: the gathered modulated input (every rank stores its rows into
+        # every copy) and the residual (every rank reduce-adds its partials into the owner's rows)
+        self.peer = PeerBuffers(self.sp, {"mg": S * H * 2, "x": n * H * 4, "sig": SIGNAL_BYTES}, dev)
+        self.mg = self.peer.local("mg", (S, H), BF16)
+        self.x = self.peer.local("x", (n, H), F32)
+        self.mg_dst = self.peer.ptrs("mg", self.sp.rank * n * H * 2)
+        self.x_dst = self.peer.ptrs("x")
+        self.sig = self.peer.ptrs("sig")
+        self.epoch = torch.zeros(1, device=dev, dtype=torch.int32)
+        self.peer_status = torch.zeros(1, device=dev, dtype=torch.int32)
+        e = lambda *s_, dt=BF16: torch.empty(*s_, device=dev, dtype=dt)  # noqa: E731
+        self.qkv_full = e(S, 3 * hd)
+        self.o_full = e(S, hd)
+        self.xq_full = e(S, hd)
+        self.xo_full = e(S, hd)
+        self.h_full = e(S, cfg.ffn_dim // P)
+        self.h = self.h[:0]  # the unsharded buffers are unused under TP
+        self.qkv = self.qkv[:0]
+
+    def _bind_attention_output(self, i):
+        pass  # TP-SP keeps its own full-sequence, local-head buffers (no attention cache)
+
+    def _rs(self, a, name, gate, flag, run_if):
+        """Row-parallel projection: this rank's partial reduce-added into the owners' residual rows."""
+        W = self.W
+        ops.gemm_gate_add_scatter(a, W[f"{name}.w"], self.x_dst, self.cfg.hidden_size, self.geo.Sv_loc,
+                                  bias=W[f"{name}.b"], gate=gate, run_flag=flag, run_if=run_if)
+        self._barrier(flag, run_if)
+
+    def _ag(self, shift, scale, kind, flag, run_if, probe=False):
+        """Sequence-parallel LN + modulation (or cast, kind 2) of this rank's rows into every rank's ``mg``."""
+        ops.norm_modulate_gather(self.x, shift, scale, self.mg_dst, self.cfg.hidden_size, self.cfg.norm_eps,
+                                 kind=kind, probe_prev=self.prev if probe else None,
+                                 probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
+        if probe:
+            self._decide()  # its barrier (carrying the rel-L1 sums) also completes the gather
+        else:
+            self._barrier(flag, run_if)
+
+    def _single_dit_block(self, i, flag, run_if, probe, ag):
+        cfg, g, W = self.cfg, self.geo, self.W
+        D, eps, hl = cfg.head_dim, cfg.qk_norm_eps, self.hl
+        hd = hl * D
+        p = f"blocks.{i}"
+        mods = self._mod(i)
+        S = g.Sv
+        # self-attention: local heads over the whole sequence
+        self._ag(mods[0], mods[1], 0, flag, run_if, probe=probe)
+        ops.gemm_qknorm_rope(self.mg, W[f"{p}.qkv.w"], self.qkv_full, hd, 2, W[f"{p}.q_norm"], W[f"{p}.k_norm"], eps,
+                             bias=W[f"{p}.qkv.b"], cos=self.cos, sin=self.sin, rope_row0=0, rope_rows=S,
+                             run_flag=flag, run_if=run_if)
+        q = self.qkv_full
+        ops.attention(q, q[:, hd:], q[:, 2 * hd:], self.o_full, hl, D, workspace=self.attn_ws, run_flag=flag,
+                      run_if=run_if)
+        self._rs(self.o_full, f"{p}.proj", mods[2], flag, run_if)
+        # cross-attention to the text (no norm before it, PixArt-alpha): gather bf16(x)
+        self._ag(None, None, 2, flag, run_if)
+        ops.gemm_qknorm_rope(self.mg, W[f"{p}.xq.w"], self.xq_full, hd, 1, W[f"{p}.xq_norm"], None, eps,
+                             bias=W[f"{p}.xq.b"], run_flag=flag, run_if=run_if)
+        kv = self.text_kv[i]
+        ops.attention(self.xq_full, kv, kv[:, hd:], self.xo_full, hl, D, workspace=self.attn_ws, run_flag=flag,
+                      run_if=run_if)
+        self._rs(self.xo_full, f"{p}.xproj", None, flag, run_if)
+        # MLP: F/P hidden columns per rank
+        self._ag(mods[3], mods[4], 0, flag, run_if)
+        ops.gemm(self.mg, W[f"{p}.fc1.w"], self.h_full, bias=W[f"{p}.fc1.b"], epilogue="gelu", run_flag=flag,
+                 run_if=run_if)
+        self._rs(self.h_full, f"{p}.fc2", mods[5], flag, run_if)
+
+
 def build_model(cfg: DiTConfig, **kw) -> DiTModel:
+    sp = kw.get("sp")
+    if sp is not None and getattr(sp, "tensor_parallel", False):
+        if cfg.family != "single-dit":
+            raise ConfigError("TP-SP is implemented for Single-DiT", "parallel.tp")
+        return SingleDiTTP(cfg, **kw)
     return (SingleDiT if cfg.family == "single-dit" else MMDiT)(cfg, **kw)

@@ -111,6 +111,33 @@ def norm_modulate(x, shift, scale, out, eps=1e-6, kind=0, probe_prev=None, probe
     return out
 
 
+def norm_modulate_gather(x, shift, scale, outs, ldy, eps=1e-6, kind=0, probe_prev=None, probe_partials=None,
+                         run_flag=None, run_if=1):
+    """norm_modulate whose rows are stored into every address in ``outs`` (device pointers with
+    stride ``ldy``, bf16): the TP-SP all-gather done by the producing kernel's own stores."""
+    _need(x, F32, "norm_modulate_gather.x")
+    rows, hidden = x.shape
+    _run("norm_modulate", rows * hidden * (4 + 2 * len(outs)) + (8 * rows * hidden if probe_prev is not None else 0),
+         "aqb_norm_modulate_gather", _p(x), x.stride(0), _p(shift), _p(scale), _native.ptr_array(outs), len(outs),
+         int(ldy), rows, hidden, float(eps), int(kind), _p(probe_prev), _p(probe_partials), _p(run_flag),
+         int(run_if), _stream())
+
+
+def gemm_gate_add_scatter(a, w, peer_out, ldo, rows_per_rank, bias=None, gate=None, run_flag=None, run_if=1):
+    """Row-parallel projection partial, gate * (a @ w.T + bias) reduce-added into the residual
+    (f32, stride ``ldo``) of the rank owning each row (``peer_out[r]``): the TP-SP reduce-scatter
+    fused into the GEMM epilogue."""
+    _need(a, BF16, "gemm_gate_add_scatter.a")
+    _need(w, BF16, "gemm_gate_add_scatter.w")
+    m, k = a.shape
+    n = w.shape[0]
+    if w.shape[1] != k:
+        raise NativeError(f"gemm_gate_add_scatter: K mismatch {k} vs {w.shape[1]}")
+    _run("gemm", 2.0 * m * n * k, "aqb_gemm_gate_add_scatter", _p(a), a.stride(0), _p(w), w.stride(0),
+         _native.ptr_array(peer_out), len(peer_out), int(ldo), int(rows_per_rank), m, n, k, _p(bias), _p(gate),
+         _p(run_flag), int(run_if), _stream())
+
+
 def gemm(a, w, out, bias=None, gate=None, epilogue="bf16", alpha=None, aux=None, run_flag=None, run_if=1):
     """out = epilogue(a @ w.T + bias) on tcgen05 (a [M,K] bf16, w [N,K] bf16).
 

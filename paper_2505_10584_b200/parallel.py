@@ -42,6 +42,8 @@ SIGNAL_BYTES = 512          # AQB_PEER_SIGNAL_BYTES
 class Ulysses:
     """Sequence-parallel group context (``P`` ranks, this rank ``rank``)."""
 
+    tensor_parallel = False
+
     def __init__(self, group=None, exchange: str | None = None):
         if not dist.is_initialized():
             raise ConfigError("torch.distributed is not initialised", "parallel.group")
@@ -89,6 +91,64 @@ class Ulysses:
             t.copy_(h)
             return
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+
+class TensorSP(Ulysses):
+    """TP-SP group (the paper's intra-node inference parallelism, ``PAPER.md:191,197,320``;
+    the reference only costs it, ``comm.py:28-53``).
+
+    Megatron-style tensor parallelism with sequence-parallel norms: the residual
+    stream stays sharded by video rows (S_v/P per rank, as under Ulysses); each
+    rank holds A/P heads of the QKV / cross-attention projections and F/P columns of
+    FFN1 (column-parallel) and the matching input columns of the out / FFN2
+    projections (row-parallel).  Per sub-layer: the sequence-parallel LayerNorm +
+    modulation stores its rows into every rank's gathered input (the all-gather is
+    the kernel's own NVLink stores, ``aqb_norm_modulate_gather``); the column-parallel
+    GEMM and attention run on the full sequence for the local heads; the row-parallel
+    GEMM's epilogue reduce-adds its partial straight into the owning rank's residual
+    rows (the reduce-scatter, ``aqb_gemm_gate_add_scatter``).  ``aqb_peer_barrier``
+    orders the steps.  No collective runs on the data path.  Single-DiT only.
+    """
+
+    tensor_parallel = True
+
+    def __init__(self, group=None):
+        super().__init__(group, exchange="p2p")
+
+    def check(self, num_heads: int, video_tokens: int, ffn_dim: int | None = None):
+        super().check(num_heads, video_tokens)
+        if ffn_dim is not None and ffn_dim % (8 * self.P):
+            raise ConfigError(f"ffn_dim {ffn_dim} not divisible into {self.P} x 8-column shards", "parallel.tp")
+
+
+def tp_shard_single_dit(W: dict, cfg, P: int, rank: int) -> dict:
+    """This rank's TP-SP slice of a Single-DiT weight dict (other entries shared, not copied).
+
+    Column-parallel (output rows): ``qkv`` (q, k, v parts: heads [rank*A/P, (rank+1)*A/P)),
+    ``xq``, ``xkv`` (k, v parts), ``fc1`` (hidden columns [rank*F/P, ...)).  Row-parallel
+    (input columns): ``proj``, ``xproj``, ``fc2``; their bias only on rank 0 (``None``
+    elsewhere: the reduce-scatter adds it once)."""
+    if cfg.num_heads % P or cfg.ffn_dim % P:
+        raise ConfigError(f"heads {cfg.num_heads} / ffn {cfg.ffn_dim} not divisible by {P}", "parallel.tp")
+    if not 0 <= rank < P:
+        raise ConfigError(f"rank {rank} outside [0, {P})", "parallel.rank")
+    hd = (cfg.num_heads // P) * cfg.head_dim
+    fl = cfg.ffn_dim // P
+    out = dict(W)
+
+    def rows(t, parts, width):  # rows [k*width*P + rank*width, +width) of each of `parts` parts
+        return torch.cat([t[k * width * P + rank * width:k * width * P + (rank + 1) * width]
+                          for k in range(parts)]).contiguous()
+
+    for i in range(cfg.num_single):
+        p = f"blocks.{i}"
+        for name, parts, width in (("qkv", 3, hd), ("xq", 1, hd), ("xkv", 2, hd), ("fc1", 1, fl)):
+            out[f"{p}.{name}.w"] = rows(W[f"{p}.{name}.w"], parts, width)
+            out[f"{p}.{name}.b"] = rows(W[f"{p}.{name}.b"], parts, width)
+        for name, width in (("proj", hd), ("xproj", hd), ("fc2", fl)):
+            out[f"{p}.{name}.w"] = W[f"{p}.{name}.w"][:, rank * width:(rank + 1) * width].contiguous()
+            out[f"{p}.{name}.b"] = W[f"{p}.{name}.b"] if rank == 0 else None
+    return out
 
 
 def oversubscribed() -> bool:

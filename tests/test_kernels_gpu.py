@@ -428,3 +428,41 @@ def test_peer_barrier_single_rank_payload():
         assert pay.tolist() == [1.5, -2.25]
     finally:
         _native.call("aqb_peer_free", ptr.value)
+
+
+# ------------------------------------------------------------------ TP-SP kernels
+@pytest.mark.parametrize("rows,hidden,kind", [(300, 2048, 0), (257, 512, 2), (975, 3072, 0)])
+def test_norm_modulate_gather_writes_every_destination(rows, hidden, kind):
+    """The fused all-gather: the same rows, bit-identical to norm_modulate, at an offset in each output."""
+    g = torch.Generator(device=dev).manual_seed(rows)
+    x = torch.randn(rows, hidden, device=dev, generator=g)
+    sh = torch.randn(hidden, device=dev, generator=g) if kind == 0 else None
+    sc = torch.randn(hidden, device=dev, generator=g) if kind == 0 else None
+    ref_o = torch.empty(rows, hidden, device=dev, dtype=torch.bfloat16)
+    ops.norm_modulate(x, sh, sc, ref_o, kind=kind)
+    P, rank = 3, 1
+    outs = [torch.full((P * rows, hidden), 7.0, device=dev, dtype=torch.bfloat16) for _ in range(P)]
+    ops.norm_modulate_gather(x, sh, sc, [o.data_ptr() + rank * rows * hidden * 2 for o in outs], hidden, kind=kind)
+    for o in outs:
+        assert torch.equal(o[rank * rows:(rank + 1) * rows], ref_o)
+        assert bool((o[:rank * rows] == 7).all()) and bool((o[(rank + 1) * rows:] == 7).all())
+
+
+@pytest.mark.parametrize("rpr,n,k", [(300, 2048, 256), (1950, 2048, 1024), (128, 512, 64), (975, 1024, 2048)])
+def test_gemm_gate_add_scatter_reduces_into_row_owners(rpr, n, k):
+    """The fused reduce-scatter: row i of gate*(A W^T + b) is added into rank i // rpr's residual
+    (blocks inside one rank by TMA reduce-add, rank-straddling blocks by red.v4); two partials sum."""
+    P = 3
+    m = P * rpr
+    g = torch.Generator(device=dev).manual_seed(rpr + n)
+    res = [torch.randn(rpr, n, device=dev, generator=g) for _ in range(P)]
+    exp = torch.cat(res).clone()
+    gate = torch.randn(n, device=dev, generator=g)
+    bias = torch.randn(n, device=dev, generator=g)
+    for part in range(2):  # two ranks' partials of a row-parallel projection
+        a = torch.randn(m, k, device=dev, generator=g).to(torch.bfloat16)
+        w = (torch.randn(n, k, device=dev, generator=g) * 0.05).to(torch.bfloat16)
+        b = bias if part == 0 else None
+        exp += gate * (a.float() @ w.float().t() + (b if b is not None else 0))
+        ops.gemm_gate_add_scatter(a, w, [r.data_ptr() for r in res], n, rpr, bias=b, gate=gate)
+    assert rel_l2(torch.cat(res), exp) < 1e-5

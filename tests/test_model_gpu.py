@@ -223,3 +223,43 @@ def test_temporal_multidiffusion_matches_oracle(name, n_prime, window, stride):
     lat = ref.denoise_windows(orcs, x0, steps, plan.clips, flags=sched.per_step_full)
     errs = [rel_l2(a, b) for a, b in zip(res.trajectory, lat[1:])]
     assert max(errs) <= TOL_BF16, errs
+
+
+def test_tp_sp_single_rank_matches_plain_model_and_oracle():
+    """TP-SP code path (fused gather / reduce-scatter kernels, peer barriers) with P = 1 in this
+    process (gloo group of one): same schedule as the plain model, within bf16 noise of it and of
+    the oracle.  Multi-rank parity: scripts/tp_check.py."""
+    import os
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2505_10584_b200.parallel import TensorSP
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        cfg = DiTConfig("single-dit", hidden_size=1024, num_heads=8, num_single=4, text_dim=256, text_len=40)
+        grid = (3, 8, 16)
+        W = init_weights(cfg, seed=0)
+        inp = synthetic_inputs(cfg, grid)
+        tp = build_model(cfg, weights=W, sp=TensorSP()).prepare(grid, inp["text"])
+        plain = build_model(cfg, weights=W).prepare(grid, inp["text"])
+        orc = ref.OracleDiT(cfg, W, inp["text"], None, grid, n_front=front_block_count(cfg.num_layers, 0.25))
+        for cache in (plan_cache(8, warmup=2, interval=2), RelL1Policy(threshold=0.06, warmup=2)):
+            r_tp = denoise(tp, inp["x0"], 8, cache, trajectory=True)
+            r_1 = denoise(plain, inp["x0"], 8, cache, trajectory=True)
+            if isinstance(cache, RelL1Policy):
+                lat, taken, _ = ref.denoise(orc, inp["x0"], 8, policy=cache)
+            else:
+                lat, taken, _ = ref.denoise(orc, inp["x0"], 8, flags=cache.per_step_full)
+            assert list(r_tp.schedule.per_step_full) == list(r_1.schedule.per_step_full) == list(taken)
+            assert max(rel_l2(a, b) for a, b in zip(r_tp.trajectory, r_1.trajectory)) < 5e-3
+            _check_traj(r_tp, lat)
+            assert tp.peer_ok()
+        tp.peer.close()
+    finally:
+        dist.destroy_process_group()

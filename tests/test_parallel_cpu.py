@@ -108,3 +108,47 @@ def test_exchange_offsets():
         exchange_offsets(8, 8, 975, 2, 128, 2048)
     with pytest.raises(ConfigError):
         exchange_offsets(0, 8, 975, 3, 128, 2048)
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_tp_shards_recombine_to_the_full_block(P):
+    """TP-SP weight slices: column-parallel outputs concatenate (per q/k/v part) and row-parallel
+    partials sum (bias once, rank 0) to the unsharded projections."""
+    from paper_2505_10584_b200.config import DiTConfig
+    from paper_2505_10584_b200.parallel import tp_shard_single_dit
+    from paper_2505_10584_b200.weights import init_weights
+
+    cfg = DiTConfig("single-dit", hidden_size=512, num_heads=4, num_single=1, text_dim=64, text_len=8)
+    W = init_weights(cfg, seed=3)
+    shards = [tp_shard_single_dit(W, cfg, P, r) for r in range(P)]
+    g = torch.Generator().manual_seed(0)
+    H, F = cfg.hidden_size, cfg.ffn_dim
+    x = torch.randn(5, H, generator=g)
+    p = "blocks.0"
+    full = x @ W[f"{p}.qkv.w"].float().t() + W[f"{p}.qkv.b"]
+    parts = [x @ s[f"{p}.qkv.w"].float().t() + s[f"{p}.qkv.b"] for s in shards]
+    hd = H // P
+    for k in range(3):  # q, k, v: rank r owns columns [k*H + r*hd, +hd)
+        got = torch.cat([pr[:, k * hd:(k + 1) * hd] for pr in parts], dim=1)
+        assert torch.allclose(got, full[:, k * H:(k + 1) * H], atol=1e-5)
+    h = torch.randn(5, F, generator=g)
+    exp = h @ W[f"{p}.fc2.w"].float().t() + W[f"{p}.fc2.b"]
+    fl = F // P
+    got = sum(h[:, r * fl:(r + 1) * fl] @ s[f"{p}.fc2.w"].float().t() + (s[f"{p}.fc2.b"] if s[f"{p}.fc2.b"] is not None
+                                                                         else 0) for r, s in enumerate(shards))
+    assert torch.allclose(got, exp, atol=1e-4)
+    assert all(s[f"{p}.proj.b"] is None for s in shards[1:]) and shards[0][f"{p}.proj.b"] is W[f"{p}.proj.b"]
+    kv = [s[f"{p}.xkv.w"] for s in shards]
+    assert torch.equal(torch.cat([k_[:hd] for k_ in kv]), W[f"{p}.xkv.w"][:H])
+    assert torch.equal(torch.cat([k_[hd:] for k_ in kv]), W[f"{p}.xkv.w"][H:])
+    assert shards[1]["t_block.w"] is W["t_block.w"]  # replicated entries are shared
+
+
+def test_tp_shard_validates():
+    from paper_2505_10584_b200.config import DiTConfig
+    from paper_2505_10584_b200.parallel import tp_shard_single_dit
+
+    cfg = DiTConfig("single-dit", hidden_size=384, num_heads=3, num_single=1, text_dim=64, text_len=8)
+    with pytest.raises(ConfigError) as e:
+        tp_shard_single_dit({}, cfg, 2, 0)
+    assert e.value.path == "parallel.tp"
