@@ -118,12 +118,7 @@ __device__ __forceinline__ void for_each_out(const OutMap& m, int head, int64_t 
   }
 }
 
-// kSplitQK: S_t(j+1) = Q_t K_{j+1}^T is issued as two N=64 halves.  Keys 0..63 land in
-// S columns 0..63, free as soon as the softmax has loaded S_t(j) into registers (it
-// signals s_free), so that half overlaps the softmax; only keys 64..127 (columns
-// 64..127, where P_t(j) lives) still wait for PV_t(j).  The per-tile critical path
-// softmax -> PV -> QK -> softmax loses half a QK.
-template <int D, uint32_t kPolyMask = kPolyMaskDefault, bool kSplitQK = true>
+template <int D, uint32_t kPolyMask = kPolyMaskDefault>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fwd_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                     const __grid_constant__ CUtensorMap tv, const __grid_constant__ OutMaps om, Params p) {
@@ -139,8 +134,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* s_full = kv_empty + C::NS;  // 2
   uint64_t* p_full = s_full + 2;        // 2
   uint64_t* o_ready = p_full + 2;       // 2
-  uint64_t* s_free = o_ready + 2;       // 2 (kSplitQK: S_t loaded into the softmax registers)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(s_free + 2);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_ready + 2);
 
   const uint32_t warp = warp_idx(), lane = lane_idx();
   const int cta = blockIdx.x;
@@ -166,7 +160,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(s_full + t, 1);
       mbar_init(p_full + t, 128);
       mbar_init(o_ready + t, 1);
-      mbar_init(s_free + t, 128);
     }
     fence_barrier_init();
   }
@@ -222,16 +215,6 @@ __global__ void __launch_bounds__(kThreads, 1)
           if (elect_one()) umma_bf16_ss(tm + t * 128, da, db, kIdescS, kk > 0);
         }
       };
-      constexpr uint32_t kIdescSH = idesc_bf16(BQ, BKV / 2, 0, 0);
-      auto issue_qk_half = [&](int t, int stage, int h) {  // keys [64h, 64h+64) -> S_t columns [64h, +64)
-        const uint32_t a0 = q_addr + t * C::kQBytes, b0 = kv_addr + stage * C::kKVBytes + h * (BKV / 2) * 128;
-#pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * (BQ * 128) + (kk & 3) * 32;
-          const uint64_t da = smem_desc(a0 + off, 0, 1024), db = smem_desc(b0 + off, 0, 1024);
-          if (elect_one()) umma_bf16_ss(tm + t * 128 + h * (BKV / 2), da, db, kIdescSH, kk > 0);
-        }
-      };
       auto issue_pv = [&](int t, int stage, bool acc) {
         // A = P_t straight from TMEM (columns 64..127 of S_t, bf16 pairs), B = V (MN-major smem)
         const uint32_t a0 = tm + t * 128 + kPCol, b0 = kv_addr + stage * C::kKVBytes;
@@ -251,15 +234,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (j < nkv) {
           mbar_wait(kv_full + ik % C::NS, (ik / C::NS) & 1);
           tc_fence_after();
-          if constexpr (kSplitQK) {
-            for (int t = 0; t < 2; ++t) {
-              if (j > 0) {
-                mbar_wait(s_free + t, (j - 1) & 1);
-                tc_fence_after();
-              }
-              issue_qk_half(t, ik % C::NS, 0);
-            }
-          }
         }
         if (j > 0) {
           mbar_wait(kv_full + iv % C::NS, (iv / C::NS) & 1);
@@ -269,10 +243,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           commit(o_ready + 0);
         }
         if (j < nkv) {
-          if constexpr (kSplitQK)
-            issue_qk_half(0, ik % C::NS, 1);
-          else
-            issue_qk(0, ik % C::NS);
+          issue_qk(0, ik % C::NS);
           commit(s_full + 0);
         }
         if (j > 0) {
@@ -283,10 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           commit(kv_empty + iv % C::NS);
         }
         if (j < nkv) {
-          if constexpr (kSplitQK)
-            issue_qk_half(1, ik % C::NS, 1);
-          else
-            issue_qk(1, ik % C::NS);
+          issue_qk(1, ik % C::NS);
           commit(s_full + 1);
           commit(kv_empty + ik % C::NS);
         }
@@ -316,10 +284,6 @@ __global__ void __launch_bounds__(kThreads, 1)
       tmem_ld64(s_tmem, sr);
       tmem_ld64(s_tmem + 64, sr + 64);
       tmem_wait_ld();
-      if constexpr (kSplitQK) {  // S_t columns 0..63 may now take the next block's first QK half
-        tc_fence_before();
-        mbar_arrive(s_free + t);
-      }
       const int kv_valid = p.seq_kv - (j0 + j) * BKV;
       if (kv_valid < BKV) {
 #pragma unroll
@@ -660,15 +624,8 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     const char* e = getenv("AQB_ATTN_POLY");
     poly = (e && !strcmp(e, "0")) ? 0 : (e && !strcmp(e, "2")) ? 2 : (e && !strcmp(e, "4")) ? 4 : 3;
   }
-  // AQB_ATTN_SPLITQK=0 (tuning): issue each QK^T whole after the previous PV
-  static int sqk = -1;
-  if (sqk < 0) {
-    const char* e = getenv("AQB_ATTN_SPLITQK");
-    sqk = (e && !strcmp(e, "0")) ? 0 : 1;
-  }
   auto kern = poly == 0 ? attn_fwd_kernel<D, 0x00> : poly == 2 ? attn_fwd_kernel<D, 0x22>
-                       : poly == 4 ? attn_fwd_kernel<D, 0x55>
-                       : sqk ? attn_fwd_kernel<D, kPolyMaskDefault, true> : attn_fwd_kernel<D, kPolyMaskDefault, false>;
+                       : poly == 4 ? attn_fwd_kernel<D, 0x55> : attn_fwd_kernel<D, kPolyMaskDefault>;
   static bool configured = false;
   if (!configured) {
     AQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
