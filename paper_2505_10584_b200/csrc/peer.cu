@@ -54,6 +54,11 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 
 __global__ void __launch_bounds__(32) barrier_kernel(BarrierArgs a) {
+  // PDL: launched while the producer drains; its writes (incl. remote TMA stores) are
+  // complete and visible from here.  Triggering at once lets the consumer's prologue
+  // overlap the spin (the consumer's own griddepcontrol.wait still waits for this kernel).
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   if (a.run_flag != nullptr && *a.run_flag != a.run_if) return;
   const int t = threadIdx.x;
   const uint32_t e = *a.epoch + 1;
@@ -157,7 +162,7 @@ int aqb_peer_barrier(void* const* peer_signal, int32_t rank, int32_t nranks, uin
   a.payload = payload, a.pay_out = pay_out, a.status = status;
   a.run_flag = run_flag, a.run_if = run_if;
   a.timeout_cycles = 20ll * 1000 * 1000 * 1000;  // ~10 s at 2 GHz
-  peer::barrier_kernel<<<1, 32, 0, reinterpret_cast<cudaStream_t>(stream)>>>(a);
+  AQB_CUDA_TRY(launch_pdl(peer::barrier_kernel, dim3(1), dim3(32), 0, reinterpret_cast<cudaStream_t>(stream), a));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }
