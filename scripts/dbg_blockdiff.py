@@ -20,7 +20,8 @@ def trace(model, rows):
         def f(*a, **kw):
             r = orig[k](*a, **kw)
             torch.cuda.synchronize()
-            snaps.append((k, model.x[:rows].clone(), model.m[:rows].clone()))
+            q = model.a2a_rcv.clone() if hasattr(model, "a2a_rcv") else model.qkv.view(model.qkv.shape[0], 3, 8, 128)[:, :, :4].clone()
+            snaps.append((k, model.x[:rows].clone(), model.m[:rows].clone(), model.o[:rows].clone(), q))
             return r
         return f
     for k in names:
@@ -42,7 +43,14 @@ if sp.rank == 0:
     s1 = trace(m1, 48)
     for i, (a, b) in enumerate(zip(s1, s2)):
         dx = float((a[1] - b[1]).abs().max()); dm = float((a[2].float() - b[2].float()).abs().max())
-        print(json.dumps({"i": i, "op1": a[0], "op2": b[0], "dx": dx, "dm": dm}), flush=True)
+        do = (a[3].float() - b[3].float()).abs()
+        bad = (do.amax(1) > 0).nonzero().flatten().tolist()
+        badc = (do.amax(0) > 0).nonzero().flatten().tolist()
+        dq = (a[4].float() - b[4].float()[:a[4].shape[0]]).abs()
+        print(json.dumps({"i": i, "op1": a[0], "op2": b[0], "dx": dx, "dm": dm, "do": float(do.max()),
+                          "dq": float(dq.max()), "dq_rows": (dq.flatten(1).amax(1) > 0).nonzero().flatten().tolist()[:10],
+                          "q_shapes": [list(a[4].shape), list(b[4].shape)],
+                          "o_bad_rows": bad[:20], "o_bad_cols": [badc[:3], badc[-3:], len(badc)]}), flush=True)
         if dx or dm:
             break
 dist.barrier()
