@@ -131,6 +131,11 @@ def main():
         res.append(attn_case(S, 256, 16, 128, args.ncu))
         if not args.ncu:
             res.append(attn_case(118800 + 256, 118800 + 256, 3, 128))  # config 4 per rank at P=8
+    if args.only == "attn-ranks":  # config-2 self-attention per rank at 1/2/4/8 GPUs, config 3/4 per rank
+        for heads in (16, 8, 4, 2):
+            res.append(attn_case(S, S, heads, 128))
+        res.append(attn_case(25440 + 256, 25440 + 256, 6, 128))
+        res.append(attn_case(118800 + 256, 118800 + 256, 3, 128))
     if args.only == "attn-long":  # config 4 per rank at P=8 (and the 1-GPU per-head shape)
         res.append(attn_case(118800 + 256, 118800 + 256, 3, 128, args.ncu))
     if args.only in ("all", "norm"):
