@@ -8,6 +8,11 @@ Public API (drop-in for the reference's cache-schedule boundary,
   ``composite_speedup``, ``ConfigError``, ``PlanningError``, ``DimensionError``
 * ``plan_vae_tiles`` / ``TilePlan`` / ``Tile`` and ``plan_temporal_windows`` /
   ``WindowPlan`` (``inference.py:89-279``), with GPU blend / Eq. 3 kernels
+* the planner formulas the path is sized by: ``ModelArch``, ``TABLE2_FIT``,
+  ``estimate_param_count``, ``flops_per_microstep``, ``tp_sp_layer_comm``,
+  ``cp_gate_and_comm`` / ``CP_TOKEN_GATE``, ``ChunkSpec`` / ``ChunkTable`` /
+  ``BUILTIN_CHUNKS`` (``config.py``, ``presets.py``, ``simulate.py``, ``comm.py``,
+  ``memory.py``; see ``planner.py``)
 * new: ``RelL1Policy``, ``DiTConfig`` + presets, ``SingleDiT`` / ``MMDiT``
   (model construction), ``denoise`` (sampler loop), ``denoise_windows``
   (temporal MultiDiffusion), ``latent_shape``, ``token_count``; multi-GPU
@@ -44,6 +49,19 @@ from .schedule import (
 )
 
 from .tiling import Tile, TilePlan, WindowPlan, plan_temporal_windows, plan_vae_tiles
+from .planner import (
+    BUILTIN_CHUNKS,
+    CP_TOKEN_GATE,
+    TABLE2_FIT,
+    ChunkSpec,
+    ChunkTable,
+    ModelArch,
+    chunk_retained_bytes,
+    cp_gate_and_comm,
+    estimate_param_count,
+    flops_per_microstep,
+    tp_sp_layer_comm,
+)
 
 __version__ = "0.1.0"
 
@@ -77,4 +95,6 @@ __all__ = [
     "SingleDiT", "MMDiT", "SingleDiTTP", "build_model", "denoise", "DenoiseResult", "denoise_windows",
     "Ulysses", "TensorSP",
     "Tile", "TilePlan", "WindowPlan", "plan_vae_tiles", "plan_temporal_windows",
+    "BUILTIN_CHUNKS", "CP_TOKEN_GATE", "TABLE2_FIT", "ChunkSpec", "ChunkTable", "ModelArch", "chunk_retained_bytes",
+    "cp_gate_and_comm", "estimate_param_count", "flops_per_microstep", "tp_sp_layer_comm",
 ]
