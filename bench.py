@@ -181,18 +181,19 @@ def _log(rank, msg):
 
 
 # --------------------------------------------------------------------------- our arm
-def mmdit_720p(sp, timed, rank):
+def mmdit_720p(sp, timed, rank, video=None, workload=None):
     """North-star companion measurement: the 13.4B MM-DiT at BASELINE config 4's geometry
     (129x720x1280 -> 118,800 video + 256 text tokens), cache on = plan_cache(50) (24 full / 26
     cached).  One full and one cached step are timed (device events, max over ranks) after one
     warm-up of each; steps/s of the 50-step video = 50 / (24 t_full + 26 t_cached).  One more
-    full step runs instrumented for the per-kernel table (joint-attention TFLOP/s)."""
+    full step runs instrumented for the per-kernel table (joint-attention TFLOP/s).
+    ``video``/``workload``: the same measurement at another geometry (config 3, 480p)."""
     from paper_2505_10584_b200 import MM_DIT_13B, build_model, flops_per_step, ops, plan_cache
     from paper_2505_10584_b200.config import VIDEO_720P_129F
     from paper_2505_10584_b200.weights import init_weights, synthetic_inputs
 
     cfg = MM_DIT_13B
-    grid = VIDEO_720P_129F.grid(cfg)
+    grid = (video or VIDEO_720P_129F).grid(cfg)
     steps = 50
     sched = plan_cache(steps)
     W = init_weights(cfg, seed=0, device="cuda")
@@ -215,8 +216,9 @@ def mmdit_720p(sp, timed, rank):
     video_ms = n_full * t_full + n_cached * t_cached
     fl = flops_per_step(cfg, grid[0] * grid[1] * grid[2])
     out = {
-        "workload": "config4: MM-DiT-13.4B (fitted H=3072 A=24, 25 dual + 29 single), 129x720x1280 -> 118,800 "
-                    "video + 256 text tokens, 50 Euler steps, cache on = plan_cache(50) (24 full / 26 cached)",
+        "workload": workload or ("config4: MM-DiT-13.4B (fitted H=3072 A=24, 25 dual + 29 single), 129x720x1280 -> "
+                                 "118,800 video + 256 text tokens, 50 Euler steps, cache on = plan_cache(50) "
+                                 "(24 full / 26 cached)"),
         "value": steps / (video_ms / 1e3), "unit": "denoise_steps/s",
         "ms_full_step": t_full, "ms_cached_step": t_cached,
         "model_tflops_full_step": fl["total"] / (t_full / 1e3) / 1e12,
@@ -362,12 +364,17 @@ def run_ours(args):
     attn_tflops = attn["work"] / (attn["ms"] / 1e3) / 1e12 if attn else None
 
     fl = flops_per_step(cfg, grid[0] * grid[1] * grid[2])
-    mm = None
+    mm = mm480 = None
     if not args.no_mmdit:
         _log(rank, "mmdit 720p")
         del model, graphs
         torch.cuda.empty_cache()
-        mm = mmdit_720p(Ulysses() if (sp and sp.tensor_parallel) else sp, timed, rank)
+        from paper_2505_10584_b200.config import VIDEO_480P_61F
+        mm_sp = Ulysses() if (sp and sp.tensor_parallel) else sp
+        mm = mmdit_720p(mm_sp, timed, rank)
+        mm480 = mmdit_720p(mm_sp, timed, rank, VIDEO_480P_61F,
+                           "config3: MM-DiT-13.4B, 61x480x848 -> 25,440 video + 256 text tokens, 50 Euler steps, "
+                           "cache on = plan_cache(50) (24 full / 26 cached)")
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -400,6 +407,7 @@ def run_ours(args):
         }
         if mm is not None:
             line["mmdit_720p"] = mm
+            line["mmdit_480p"] = mm480
         if world == 1 and not args.no_cpu:
             threads = os.cpu_count() or 1
             c = cpu_reference_sample(threads)
