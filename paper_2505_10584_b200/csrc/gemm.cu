@@ -50,6 +50,10 @@ constexpr int kEpiGateAdd = 100;
 // block that lies in one rank's rows, per-thread red.global.add.v4 for a block that
 // straddles two ranks.
 constexpr int kEpiGateAddScatter = 101;
+// Internal: the QK-norm epilogue without RoPE (cross-attention q, text rows): no shared
+// RoPE tiles, so the pair kernel keeps its full pipeline depth.
+constexpr int kEpiQkNoRope = 102;
+__host__ __device__ constexpr bool is_qk(int epi) { return epi == AQB_EPI_QKNORM_ROPE || epi == kEpiQkNoRope; }
 constexpr int kEpiBuf = 128 * 128;  // one epilogue chunk: 128 rows x 128 B
 constexpr int kAuxBuf = 128 * 64;   // bf16 copy of a gate*residual chunk: 128 rows x 64 B (64B swizzle)
 
@@ -90,6 +94,7 @@ constexpr int kMaxPeers = 8;
 struct PeerMaps {
   CUtensorMap m[kMaxPeers];
   CUtensorMap bh;  // W with a BN/4-row box: the half-width tail units of the pair kernel
+  CUtensorMap rcos, rsin;  // QK-norm + RoPE epilogue: [rope_rows, 64] f32 tables, 32 x 128-row boxes
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int t, int& mb, int& nb) {
@@ -168,6 +173,12 @@ struct EpiState {
   uint32_t tiles_done;   // tile_iter of the tile being drained
   uint32_t issued;       // residual chunks requested so far (idx < issued)
   uint32_t phase_bits;   // per-buffer mbarrier parity (loads happen only for valid chunks)
+  // QK-norm + RoPE (pair kernel): the tile's 128 rows of the cos / sin tables, TMA-loaded
+  // into shared memory (cos lo|hi, sin lo|hi: 4 x [128 rows][128 B], 128B-swizzled) while
+  // the accumulator fills, instead of per-row global loads in the epilogue
+  uint8_t* rope;         // nullptr: global loads
+  uint64_t* rbar;
+  uint32_t rphase;
 };
 
 constexpr int kSmemMax = 232448;
@@ -199,6 +210,20 @@ constexpr int res_stages() {
 template <int EPI>
 constexpr int aux_bytes() { return EPI == AQB_EPI_GATE_RES ? 2 * kAuxBuf : 0; }
 
+// shared-memory RoPE tables of the QK-norm epilogue (pair kernel only)
+template <int EPI, bool PAIR>
+constexpr int rope_bytes() { return (EPI == AQB_EPI_QKNORM_ROPE && PAIR) ? 4 * kEpiBuf : 0; }
+
+// pipeline stages of the QK-norm variant: the most that leave room for the RoPE tiles
+template <int BN, int STAGES, bool PAIR>
+constexpr int qk_stages() {
+  for (int s = STAGES; s > 2; --s)
+    if (s * stage_bytes<BN, PAIR>() + 2 * kEpiBuf + rope_bytes<AQB_EPI_QKNORM_ROPE, PAIR>() + 1024 + 256 <=
+        kSmemMax)
+      return s;
+  return 2;
+}
+
 template <int EPI>
 constexpr int epi_cols() {
   return (EPI == AQB_EPI_F32 || EPI == AQB_EPI_GATE_RES || EPI == kEpiGateAdd || EPI == kEpiGateAddScatter) ? 32 : 64;
@@ -224,8 +249,19 @@ __device__ __forceinline__ void res_request(const Params& p, const CUtensorMap* 
 // Residual prefetch before the first tile's accumulator wait, so the stream's
 // start-up latency hides behind the first tile's MMAs.
 template <int EPI, int BN, int NB>
-__device__ __forceinline__ void epilogue_prologue(const Params& p, const CUtensorMap* tmo, EpiState& es,
-                                                  bool leader_thread) {
+__device__ __forceinline__ void epilogue_prologue(const Params& p, const CUtensorMap* tmo, const PeerMaps* pm,
+                                                  EpiState& es, int row0, bool leader_thread) {
+  if constexpr (is_qk(EPI)) {
+    // the previous tile's epilogue ended with a named barrier: the rope buffer is free
+    if (es.rope != nullptr && leader_thread && p.rope_row0 + row0 < p.rope_rows) {
+      mbar_arrive_expect_tx(es.rbar, 4 * kEpiBuf);
+      const int y = int(p.rope_row0 + row0);
+      tma_load_2d(es.rope + 0 * kEpiBuf, &pm->rcos, es.rbar, 0, y, kEvictNormal);
+      tma_load_2d(es.rope + 1 * kEpiBuf, &pm->rcos, es.rbar, 32, y, kEvictNormal);
+      tma_load_2d(es.rope + 2 * kEpiBuf, &pm->rsin, es.rbar, 0, y, kEvictNormal);
+      tma_load_2d(es.rope + 3 * kEpiBuf, &pm->rsin, es.rbar, 32, y, kEvictNormal);
+    }
+  }
   if constexpr (EPI == AQB_EPI_GATE_RES) {
     if (es.issued == 0) {
       if (leader_thread)
@@ -253,10 +289,17 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
       euler_chunk(p, row0 + r, col_base + c, u);
     }
     return;
-  } else if constexpr (EPI == AQB_EPI_QKNORM_ROPE) {
+  } else if constexpr (is_qk(EPI)) {
     // One 128-column head at a time: RMS-norm (+ RoPE) in registers, then two
     // 64-column chunks through the swizzled smem buffers and a 5-D TMA store
     // that lands in the [group][row][part][head][128] layout (natural or packed).
+    const bool rope_tile = p.rope_row0 + row0 < p.rope_rows;  // CTA-uniform
+    const bool rope_smem = es.rope != nullptr && rope_tile;
+    if (rope_smem) {
+      mbar_wait(es.rbar, es.rphase);
+      es.rphase ^= 1;
+    }
+    const uint32_t rope_row = smem_u32(es.rope) + r * 128, rsw = r & 7;
 #pragma unroll 1
     for (int hc = 0; hc < BN; hc += 128) {
       const int colh = col_base + hc;
@@ -301,7 +344,15 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           const float4* s4 = reinterpret_cast<const float4*>(p.rope_sin + grow * 64);
 #pragma unroll
           for (int i = 0; i < 16; ++i) {
-            const float4 cc = __ldg(c4 + i), sn = __ldg(s4 + i);
+            float4 cc, sn;
+            if (rope_smem) {  // float4 i of the row: box i/8, 16-byte chunk i%8 (128B swizzle)
+              const uint32_t off = rope_row + (i >> 3) * kEpiBuf + ((((i & 7) ^ rsw)) << 4);
+              const uint4 a = lds128(off), b = lds128(off + 2 * kEpiBuf);
+              cc = make_float4(__uint_as_float(a.x), __uint_as_float(a.y), __uint_as_float(a.z), __uint_as_float(a.w));
+              sn = make_float4(__uint_as_float(b.x), __uint_as_float(b.y), __uint_as_float(b.z), __uint_as_float(b.w));
+            } else {
+              cc = __ldg(c4 + i), sn = __ldg(s4 + i);
+            }
             const float cs[4] = {cc.x, cc.y, cc.z, cc.w}, sv[4] = {sn.x, sn.y, sn.z, sn.w};
 #pragma unroll
             for (int j = 0; j < 4; ++j) {
@@ -339,6 +390,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
         ++es.chunk;
       }
     }
+    if (es.rope != nullptr) named_bar_sync(1, 128);  // every row's RoPE read: the next tile may reload
   } else {
     constexpr int CW = epi_cols<EPI>();  // columns per 128-byte chunk
 #pragma unroll 1
@@ -490,6 +542,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 template <int BN, int STAGES, bool PAIR, int EPI>
 constexpr int smem_bytes() {
   return STAGES * (BM + (PAIR ? BN / 2 : BN)) * BK * 2 + epi_bufs<BN, STAGES, PAIR, EPI>() * kEpiBuf + aux_bytes<EPI>() +
+         rope_bytes<EPI, PAIR>() +
          1024 /*align*/ + 256 /*bars*/;
 }
 
@@ -508,7 +561,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* ebar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + NB);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + NB + 1);  // ebar[NB]: rope barrier slot (unused here)
 
   constexpr uint32_t kTmemCols = 2 * BN;
   const uint32_t warp = warp_idx(), lane = lane_idx();
@@ -526,6 +579,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(tempty + a, 4);
     }
     for (int b = 0; b < NB; ++b) mbar_init(ebar + b, 1);
+    mbar_init(ebar + NB, 1);  // rope tables (QK-norm epilogue)
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, kTmemCols);
@@ -587,13 +641,13 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;  // TMEM lane quadrant this warp may access
-    EpiState es{ebuf, ebar, 0, int(blockIdx.x), int(gridDim.x), BM, 0, 0, 0, 0};
+    EpiState es{ebuf, ebar, 0, int(blockIdx.x), int(gridDim.x), BM, 0, 0, 0, 0, nullptr, nullptr, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int t = blockIdx.x; t < p.num_units; t += gridDim.x) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
-      epilogue_prologue<EPI, BN, NB>(p, &tma_o, es, q == 0 && lane == 0);
+      epilogue_prologue<EPI, BN, NB>(p, &tma_o, &pm, es, mb * BM, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       epilogue_tile<EPI, BN, NB>(p, &tma_o, &pm, es, tmem + acc * BN, mb * BM, nb * BN, BN, q, lane);
@@ -625,12 +679,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sb = base + STAGES * kABytes;
   uint8_t* ebuf = base + STAGES * (kABytes + kBBytes);
   constexpr int NB = epi_bufs<BN, STAGES, true, EPI>();
-  uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + NB * kEpiBuf + aux_bytes<EPI>());
+  uint8_t* rope_buf = ebuf + NB * kEpiBuf + aux_bytes<EPI>();  // rope_bytes<EPI, true>() (QK-norm only)
+  uint64_t* full = reinterpret_cast<uint64_t*>(rope_buf + rope_bytes<EPI, true>());
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + 2;
   uint64_t* ebar = tempty + 2;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(ebar + NB);
+  uint64_t* rbar = ebar + NB;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(rbar + 1);
 
   constexpr uint32_t kTmemCols = 2 * BN;
   const uint32_t warp = warp_idx(), lane = lane_idx();
@@ -651,6 +707,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       mbar_init(tempty + a, 8);  // 4 epilogue warps x 2 CTAs (used on the leader)
     }
     for (int b = 0; b < NB; ++b) mbar_init(ebar + b, 1);
+    mbar_init(ebar + NB, 1);  // rope tables (QK-norm epilogue)
     fence_barrier_init();
   }
   cluster_sync();
@@ -725,13 +782,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     }
   } else if (warp >= 4) {
     const uint32_t q = warp & 3;
-    EpiState es{ebuf, ebar, 0, cluster, nclusters, 2 * BM, int(rank) * BM, 0, 0, 0};
+    EpiState es{ebuf, ebar, 0, cluster, nclusters, 2 * BM, int(rank) * BM, 0, 0, 0,
+                rope_bytes<EPI, true>() ? rope_buf : nullptr, rbar, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
     for (int u = cluster; u < p.num_units; u += nclusters) {
       int mb, col0, width;
       unit_coords<BN>(p, u, mb, col0, width);
-      epilogue_prologue<EPI, BN, NB>(p, &tma_o, es, q == 0 && lane == 0);
+      epilogue_prologue<EPI, BN, NB>(p, &tma_o, &pm, es, mb * (2 * BM) + int(rank) * BM, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       epilogue_tile<EPI, BN, NB>(p, &tma_o, &pm, es, tmem + acc * BN, mb * (2 * BM) + rank * BM, col0, width, q,
@@ -793,7 +851,8 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
     case kEpiGateAdd: return launch<BN, STAGES, kEpiGateAdd, PAIR>(ta, tb, to, pm, p, s);
     case kEpiGateAddScatter: return launch<BN, STAGES, kEpiGateAddScatter, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_EULER: return launch<BN, STAGES, AQB_EPI_EULER, PAIR>(ta, tb, to, pm, p, s);
-    case AQB_EPI_QKNORM_ROPE: return launch<BN, STAGES, AQB_EPI_QKNORM_ROPE, PAIR>(ta, tb, to, pm, p, s);
+    case AQB_EPI_QKNORM_ROPE: return launch<BN, qk_stages<BN, STAGES, PAIR>(), AQB_EPI_QKNORM_ROPE, PAIR>(ta, tb, to, pm, p, s);
+    case kEpiQkNoRope: return launch<BN, STAGES, kEpiQkNoRope, PAIR>(ta, tb, to, pm, p, s);
   }
   return set_error(AQB_EINVAL, "unknown epilogue %d", epi);
 }
@@ -1031,8 +1090,21 @@ static int qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw, i
   p.rope_row0 = rope_row0, p.rope_rows = rope_rows, p.part_width = part_width, p.norm_parts = norm_parts;
   p.hpg = hpg, p.g_base = g_base, p.groups = groups, p.eps = eps;
   p.peer_groups = peer_out != nullptr;
-  return run(a, lda, w, ldw, m, n, k, AQB_EPI_QKNORM_ROPE, p, to, pick_variant(m, n, k), stream,
-             peer_out ? &pm : nullptr);
+  if (rope_rows > 0) {  // cos / sin tables for the pair kernel's TMA-staged RoPE
+    AQB_CHECK_ARG(reinterpret_cast<uintptr_t>(rope_cos) % 16 == 0 && reinterpret_cast<uintptr_t>(rope_sin) % 16 == 0,
+                  "gemm_qknorm_rope: rope tables must be 16B aligned");
+    const uint64_t dims[2] = {64, uint64_t(rope_rows)};
+    const uint64_t strides[1] = {256};
+    const uint32_t box[2] = {32, uint32_t(BM)};
+    int rc = make_tmap(&pm.rcos, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rope_cos, 2, dims, strides, box,
+                       CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+    rc = make_tmap(&pm.rsin, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, rope_sin, 2, dims, strides, box,
+                   CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  return run(a, lda, w, ldw, m, n, k, rope_rows > 0 ? AQB_EPI_QKNORM_ROPE : kEpiQkNoRope, p, to,
+             pick_variant(m, n, k), stream, &pm);
 }
 
 }  // namespace gemm

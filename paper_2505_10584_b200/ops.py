@@ -38,10 +38,20 @@ class KernelProfiler:
         self.records = []
         self.count = 0
 
+    def by_launch(self):
+        """Per (C-ABI entry, work) group — i.e. per shape — launches, ms and work."""
+        torch.cuda.synchronize()
+        out = {}
+        for _kind, e0, e1, work, name in self.records:
+            d = out.setdefault((name, work), {"launches": 0, "ms": 0.0})
+            d["launches"] += 1
+            d["ms"] += e0.elapsed_time(e1)
+        return out
+
     def summary(self):
         torch.cuda.synchronize()
         out = {}
-        for kind, e0, e1, work in self.records:
+        for kind, e0, e1, work, _name in self.records:
             d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "work": 0.0})
             d["launches"] += 1
             d["ms"] += e0.elapsed_time(e1)
@@ -81,7 +91,7 @@ def _run(kind, work, name, *args):
     e0.record()
     _native.call(name, *args)
     e1.record()
-    prof.records.append((kind, e0, e1, float(work)))
+    prof.records.append((kind, e0, e1, float(work), name))
 
 
 def _p(t):

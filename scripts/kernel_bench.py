@@ -64,6 +64,26 @@ def gemm_case(m, n, k, epi="bf16", ncu=False):
     return {"kernel": "gemm", "m": m, "n": n, "k": k, "epi": epi, "ms": ms, "tflops": 2 * m * n * k / ms / 1e9}
 
 
+def qkv_fused_case(m, heads, k, ncu=False, parts=3, norm_parts=2, rope=True):
+    """The QKV projection with the QK-RMSNorm + 3D-RoPE epilogue (as in the model)."""
+    d = 128
+    n = parts * heads * d
+    a = torch.randn(m, k, device=dev).to(torch.bfloat16)
+    w = (torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)
+    b = torch.randn(n, device=dev)
+    qw, kw = torch.ones(d, device=dev), torch.ones(d, device=dev)
+    cos, sin = torch.randn(m, d // 2, device=dev), torch.randn(m, d // 2, device=dev)
+    out = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+    fn = lambda: ops.gemm_qknorm_rope(a, w, out, heads * d, norm_parts, qw, kw, 1e-6, bias=b, cos=cos, sin=sin,  # noqa: E731
+                                      rope_row0=0, rope_rows=m if rope else 0)
+    if ncu:
+        fn()
+        return None
+    ms = timeit(fn)
+    return {"kernel": "gemm_qknorm_rope", "m": m, "n": n, "k": k, "norm_parts": norm_parts, "rope": rope, "ms": ms,
+            "tflops": 2 * m * n * k / ms / 1e9}
+
+
 def attn_case(sq, skv, heads, d=128, ncu=False, packed=True):
     qkv = torch.randn(max(sq, skv), 3 * heads * d, device=dev).to(torch.bfloat16)
     o = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
@@ -131,6 +151,14 @@ def main():
         res.append(attn_case(S, 256, 16, 128, args.ncu))
         if not args.ncu:
             res.append(attn_case(118800 + 256, 118800 + 256, 3, 128))  # config 4 per rank at P=8
+    if args.only == "qkv":  # fused QKV epilogue vs the plain bf16 epilogue, config 2 and shards
+        for m in (S, S // 2, S // 4):
+            res.append(gemm_case(m, 3 * H, H, "bf16", args.ncu))
+            res.append(qkv_fused_case(m, 16, H, args.ncu))
+        res.append(qkv_fused_case(S, 16, H, args.ncu, parts=1, norm_parts=1))  # cross-attention q
+        if not args.ncu:  # epilogue cost breakdown: without RoPE, without norm
+            res.append(qkv_fused_case(S, 16, H, rope=False))
+            res.append(qkv_fused_case(S, 16, H, norm_parts=0, rope=False))
     if args.only == "attn-ranks":  # config-2 self-attention per rank at 1/2/4/8 GPUs, config 3/4 per rank
         for heads in (16, 8, 4, 2):
             res.append(attn_case(S, S, heads, 128))
