@@ -64,6 +64,29 @@ def gemm_case(m, n, k, epi="bf16", ncu=False):
     return {"kernel": "gemm", "m": m, "n": n, "k": k, "epi": epi, "ms": ms, "tflops": 2 * m * n * k / ms / 1e9}
 
 
+def proj_aux_case(m, n, k, split=False, ncu=False):
+    """Single-DiT self-attention out-projection: x += gate*(o W^T + b) and bf16(x) for the
+    cross-attention q — fused (gate*residual + bf16 copy) or split (TMA reduce-add GEMM + cast)."""
+    a = torch.randn(m, k, device=dev).to(torch.bfloat16)
+    w = (torch.randn(n, k, device=dev) * 0.02).to(torch.bfloat16)
+    b = torch.randn(n, device=dev)
+    g = torch.randn(n, device=dev)
+    x = torch.randn(m, n, device=dev)
+    aux = torch.empty(m, n, device=dev, dtype=torch.bfloat16)
+    if split:
+        def fn():
+            ops.gemm(a, w, x, bias=b, gate=g, epilogue="gate_res")
+            ops.norm_modulate(x, None, None, aux, kind=2)
+    else:
+        fn = lambda: ops.gemm(a, w, x, bias=b, gate=g, epilogue="gate_res", aux=aux)  # noqa: E731
+    if ncu:
+        fn()
+        return None
+    ms = timeit(fn)
+    return {"kernel": "proj+bf16(x)", "split": split, "m": m, "n": n, "k": k, "ms": ms,
+            "tflops": 2 * m * n * k / ms / 1e9}
+
+
 def qkv_fused_case(m, heads, k, ncu=False, parts=3, norm_parts=2, rope=True):
     """The QKV projection with the QK-RMSNorm + 3D-RoPE epilogue (as in the model)."""
     d = 128
@@ -159,6 +182,10 @@ def main():
         if not args.ncu:  # epilogue cost breakdown: without RoPE, without norm
             res.append(qkv_fused_case(S, 16, H, rope=False))
             res.append(qkv_fused_case(S, 16, H, norm_parts=0, rope=False))
+    if args.only == "proj":
+        for m in (S, S // 2, S // 4):
+            res.append(proj_aux_case(m, H, H))
+            res.append(proj_aux_case(m, H, H, split=True))
     if args.only == "attn-ranks":  # config-2 self-attention per rank at 1/2/4/8 GPUs, config 3/4 per rank
         for heads in (16, 8, 4, 2):
             res.append(attn_case(S, S, heads, 128))
