@@ -63,12 +63,14 @@ __global__ void __launch_bounds__(32) barrier_kernel(BarrierArgs a) {
   const int t = threadIdx.x;
   const uint32_t e = *a.epoch + 1;
   const int par = e & 1;
-  // every prior write of this rank (previous kernels, incl. remote TMA stores) before the signal
-  __threadfence_system();
+  // every prior write of this rank (previous kernels, incl. remote TMA stores — complete
+  // before those kernels exited, and visible here after griddepcontrol.wait) is ordered
+  // before the signal: an acq_rel system fence (cumulative), then a release store, which
+  // also orders this thread's payload writes
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
   if (t < a.nranks) {
     Signal* dst = a.sig[t];
     for (int i = 0; i < a.npay; ++i) dst->pay[par][a.rank][i] = a.payload[i];
-    __threadfence_system();
     st_release_sys(&dst->flag[a.rank], e);
   }
   if (t < a.nranks) {

@@ -211,6 +211,45 @@ def blend_tiles(plan: TilePlan, tiles, out: torch.Tensor) -> torch.Tensor:
     return out
 
 
+class PeerTiles:
+    """Parallel VAE decode across the GPUs of one box (``PAPER.md:79,318``; plan
+    ``inference.py:189-226``): rank r decodes the tiles ``plan.tiles_of(r)`` into its slots
+    of a symmetric peer buffer, and :meth:`blend` on any rank reads every tile straight
+    from its owner's memory over NVLink (``aqb_tile_blend`` takes per-tile device
+    addresses), so the blended latent needs no gather.  Collective construction (every
+    rank, same plan and channel count)."""
+
+    def __init__(self, plan: TilePlan, sp, channels: int, device="cuda"):
+        from .parallel import PeerBuffers
+
+        if plan.devices != sp.P:
+            raise ConfigError(f"plan for {plan.devices} devices, group of {sp.P}", "vae.devices")
+        self.plan, self.sp, self.channels = plan, sp, channels
+        self.tile_elems = channels * int(np.prod(plan.tiles[0].size))
+        self.slots = [plan.tiles_of(r) for r in range(sp.P)]
+        per_rank = max(len(s) for s in self.slots)
+        self.peer = PeerBuffers(sp, {"tiles": per_rank * self.tile_elems * 4}, device)
+        self._local = self.peer.local("tiles", (per_rank, channels, *plan.tiles[0].size), torch.float32)
+        base = self.peer.ptrs("tiles")
+        self._ptrs = [0] * len(plan.tiles)
+        for r, idx in enumerate(self.slots):
+            for j, i in enumerate(idx):
+                self._ptrs[i] = base[r] + j * self.tile_elems * 4
+
+    def local_tile(self, i: int) -> torch.Tensor:
+        """This rank's buffer for plan tile ``i`` (must be one of ``plan.tiles_of(rank)``)."""
+        j = self.slots[self.sp.rank].index(i)
+        return self._local[j]
+
+    def blend(self, out: torch.Tensor) -> torch.Tensor:
+        """Blend every rank's tiles into ``out`` [C, *latent] (after all ranks wrote theirs:
+        the caller orders it, e.g. ``torch.distributed.barrier`` after a device sync)."""
+        return blend_tiles(self.plan, self._ptrs, out)
+
+    def close(self):
+        self.peer.close()
+
+
 def average_windows(plan: WindowPlan, clips, out: torch.Tensor) -> torch.Tensor:
     """Eq. 3 on the GPU: out[c, i] = (sum_{k in S(i)} clip_k[c, i - s_k]) / |S(i)|.
 
