@@ -370,7 +370,7 @@ def run_ours(args):
         del model, graphs
         torch.cuda.empty_cache()
         from paper_2505_10584_b200.config import VIDEO_480P_61F
-        mm_sp = Ulysses() if (sp and sp.tensor_parallel) else sp
+        mm_sp = sp  # TP-SP (--parallel tp) covers both families
         mm = mmdit_720p(mm_sp, timed, rank)
         mm480 = mmdit_720p(mm_sp, timed, rank, VIDEO_480P_61F,
                            "config3: MM-DiT-13.4B, 61x480x848 -> 25,440 video + 256 text tokens, 50 Euler steps, "
@@ -450,8 +450,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-mmdit", action="store_true", help="skip the 13.4B MM-DiT 720p companion measurement")
     ap.add_argument("--parallel", choices=["ulysses", "tp"], default="ulysses",
-                    help="N>1: Ulysses sequence parallel (default) or TP-SP (Single-DiT; the MM-DiT companion "
-                         "then runs Ulysses)")
+                    help="N>1: Ulysses sequence parallel (default) or TP-SP (both families)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -72,6 +72,15 @@ int aqb_gemm_gate_add_scatter(const void* a, int64_t lda, const void* w, int64_t
                               int32_t nranks, int64_t ldo, int64_t rows_per_rank, int64_t m, int64_t n, int64_t k,
                               const float* bias, const float* gate, const int32_t* run_flag, int32_t run_if,
                               void* stream);
+/* TP-SP all-reduce of replicated rows (MM-DiT text rows), deterministic:
+ * aqb_gate_bcast writes gate[c] * src[r, c] (gate NULL: 1) into each of the ndst
+ * (1..8) buffers dst[d] + r*ldd (this rank's slot in every rank's slot buffer, over
+ * NVLink); after a barrier aqb_sum_slots adds the nslots slots (slot k at
+ * slots + k*slot_stride, row stride lds) into x in slot order.  f32, cols % 4 == 0. */
+int aqb_gate_bcast(const float* src, int64_t lds, const float* gate, float* const* dst, int32_t ndst, int64_t ldd,
+                   int64_t rows, int64_t cols, const int32_t* run_flag, int32_t run_if, void* stream);
+int aqb_sum_slots(float* x, int64_t ldx, const float* slots, int32_t nslots, int64_t slot_stride, int64_t lds,
+                  int64_t rows, int64_t cols, const int32_t* run_flag, int32_t run_if, void* stream);
 int aqb_norm_modulate_gather(const float* x, int64_t ldx, const float* shift, const float* scale, void* const* y,
                              int32_t ny, int64_t ldy, int64_t rows, int32_t hidden, float eps, int32_t norm_kind,
                              float* probe_prev, float* probe_partials, const int32_t* run_flag, int32_t run_if,

@@ -321,6 +321,57 @@ __global__ void add_bcast_kernel(float* out, const float* a, int64_t period, con
     out[i] = a[i % period] + b[i];
 }
 
+// ------------------------------------------------------- TP-SP replicated rows
+// The text rows of an MM-DiT under TP-SP are replicated on every rank, so their
+// row-parallel projections need an all-reduce.  Deterministically: every rank writes
+// gate * partial into slot `rank` of every rank's slot buffer (peer stores), then after
+// the barrier each rank adds its P slots in rank order (identical bits everywhere).
+struct SlotDsts {
+  float* p[8];
+  int n;
+};
+
+__global__ void gate_bcast_kernel(const float* __restrict__ src, int64_t lds, const float* __restrict__ gate,
+                                  SlotDsts dst, int64_t ldd, int64_t rows, int cols4, const int32_t* flag,
+                                  int32_t run_if) {
+  pdl_wait();
+  pdl_trigger();
+  if (!gate_open(flag, run_if)) return;
+  const int64_t total = rows * cols4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols4;
+    const int c = int(i % cols4);
+    float4 v = *reinterpret_cast<const float4*>(src + r * lds + 4 * c);
+    if (gate) {
+      const float4 g = __ldg(reinterpret_cast<const float4*>(gate) + c);
+      v.x *= g.x, v.y *= g.y, v.z *= g.z, v.w *= g.w;
+    }
+#pragma unroll 1
+    for (int d = 0; d < dst.n; ++d) *reinterpret_cast<float4*>(dst.p[d] + r * ldd + 4 * c) = v;
+  }
+}
+
+__global__ void sum_slots_kernel(float* __restrict__ x, int64_t ldx, const float* __restrict__ slots, int nslots,
+                                 int64_t slot_stride, int64_t lds, int64_t rows, int cols4, const int32_t* flag,
+                                 int32_t run_if) {
+  pdl_wait();
+  pdl_trigger();
+  if (!gate_open(flag, run_if)) return;
+  const int64_t total = rows * cols4;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < total;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t r = i / cols4;
+    const int c = int(i % cols4);
+    float4 a = *reinterpret_cast<const float4*>(x + r * ldx + 4 * c);
+    for (int k = 0; k < nslots; ++k) {  // rank order
+      const float4 b = *reinterpret_cast<const float4*>(slots + k * slot_stride + r * lds + 4 * c);
+      a.x += b.x, a.y += b.y, a.z += b.z, a.w += b.w;
+    }
+    *reinterpret_cast<float4*>(x + r * ldx + 4 * c) = a;
+  }
+}
+
 // ------------------------------------------------------- diffusion cache
 __global__ void __launch_bounds__(1024) rel_l1_reduce_kernel(const float* partials, int64_t rows, float* sums) {
   pdl_wait();  // PDL: predecessor's writes visible from here
@@ -630,6 +681,38 @@ extern "C" int aqb_add_bcast(float* out, const float* a, int64_t period, const f
   AQB_CHECK_ARG(out && a && b && period >= 1, "add_bcast: bad args");
   if (n <= 0) return AQB_OK;
   AQB_CUDA_TRY(launch_pdl(add_bcast_kernel, dim3(grid_for(n, 256)), dim3(256), 0, reinterpret_cast<cudaStream_t>(stream), out, a, period, b, n));
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_gate_bcast(const float* src, int64_t lds, const float* gate, float* const* dst, int32_t ndst,
+                              int64_t ldd, int64_t rows, int64_t cols, const int32_t* run_flag, int32_t run_if,
+                              void* stream) {
+  AQB_CHECK_ARG(src && dst && ndst >= 1 && ndst <= 8 && cols % 4 == 0 && lds % 4 == 0 && ldd % 4 == 0,
+                "gate_bcast: bad args");
+  SlotDsts d{};
+  d.n = ndst;
+  for (int i = 0; i < ndst; ++i) {
+    AQB_CHECK_ARG(dst[i] && reinterpret_cast<uintptr_t>(dst[i]) % 16 == 0, "gate_bcast: dst[%d]", i);
+    d.p[i] = dst[i];
+  }
+  if (rows <= 0) return AQB_OK;
+  AQB_CUDA_TRY(launch_pdl(gate_bcast_kernel, dim3(grid_for(rows * cols / 4, 256)), dim3(256), 0,
+                          reinterpret_cast<cudaStream_t>(stream), src, lds, gate, d, ldd, rows, int(cols / 4),
+                          run_flag, run_if));
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+extern "C" int aqb_sum_slots(float* x, int64_t ldx, const float* slots, int32_t nslots, int64_t slot_stride,
+                             int64_t lds, int64_t rows, int64_t cols, const int32_t* run_flag, int32_t run_if,
+                             void* stream) {
+  AQB_CHECK_ARG(x && slots && nslots >= 1 && cols % 4 == 0 && ldx % 4 == 0 && lds % 4 == 0 && slot_stride % 4 == 0,
+                "sum_slots: bad args");
+  if (rows <= 0) return AQB_OK;
+  AQB_CUDA_TRY(launch_pdl(sum_slots_kernel, dim3(grid_for(rows * cols / 4, 256)), dim3(256), 0,
+                          reinterpret_cast<cudaStream_t>(stream), x, ldx, slots, nslots, slot_stride, lds, rows,
+                          int(cols / 4), run_flag, run_if));
   AQB_LAUNCH_CHECK();
   return AQB_OK;
 }

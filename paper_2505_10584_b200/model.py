@@ -37,7 +37,7 @@ import torch
 from . import ops
 from .config import DiTConfig
 from .errors import ConfigError
-from .parallel import SIGNAL_BYTES, PeerBuffers, Ulysses, exchange_offsets, tp_shard_single_dit
+from .parallel import SIGNAL_BYTES, PeerBuffers, Ulysses, exchange_offsets, tp_shard
 from .schedule import front_block_count
 from .weights import init_weights
 
@@ -225,7 +225,7 @@ class DiTModel:
         return self.sp is not None and getattr(self.sp, "tensor_parallel", False)
 
     def _prepare_tp(self):
-        raise ConfigError("TP-SP is implemented for Single-DiT", "parallel.tp")
+        raise ConfigError("TP-SP needs a TP model class (build_model with a TensorSP group)", "parallel.tp")
 
     def _barrier(self, flag=None, run_if=1, payload=None):
         ops.peer_barrier(self.sig, self.sp.rank, self.epoch, self.peer_status, payload=payload,
@@ -655,78 +655,111 @@ class MMDiT(DiTModel):
         super().__init__(cfg, **kw)
 
 
-class SingleDiTTP(SingleDiT):
-    """Single-DiT under TP-SP (:class:`~paper_2505_10584_b200.parallel.TensorSP`).
+class _TensorParallel:
+    """TP-SP machinery shared by both families (:class:`~paper_2505_10584_b200.parallel.TensorSP`).
 
-    Weights are sharded at construction (:func:`~paper_2505_10584_b200.parallel.tp_shard_single_dit`):
-    QKV / cross-attention q and text K/V / FFN1 by output rows (this rank's A/P heads, F/P
-    hidden columns), the out / cross-out / FFN2 projections by input columns (their bias on
-    rank 0 only).  AdaLN tables, timestep MLP, patch embed and final layer are replicated.
-    Per block, six sub-steps each end in ``aqb_peer_barrier``:
+    Weights are sharded at construction (:func:`~paper_2505_10584_b200.parallel.tp_shard`):
+    QKV / FFN1 (and Single-DiT's cross-attention q and text K/V) by output rows — this
+    rank's A/P heads and F/P hidden columns — and the out / FFN2 (/ cross-out) projections
+    by input columns, their bias on rank 0 only.  AdaLN, timestep / pooled MLPs, patch
+    embed and final layer are replicated.  Each sub-layer is
 
-      AG(LN+mod(x))  -> QKV(local heads, all rows) -> attention -> proj  -> RS into x
-      AG(bf16 x)     -> q(local heads) -> cross-attention to text -> proj -> RS into x
-      AG(LN+mod(x))  -> FFN1(local columns, GeLU) -> FFN2 -> RS into x
+      AG(LN+mod of this rank's video rows) -> column-parallel GEMM(s) on all rows
+      [-> attention over the local heads]  -> row-parallel GEMM -> RS into x
 
-    The reduce-scatter sums float32 partials at the owning rank in arrival order, so a
-    run is reproducible only to rounding (not bitwise) — unlike the Ulysses path.
+    with the all-gather stored by the LN kernel into every rank (``aqb_norm_modulate_gather``),
+    the reduce-scatter reduce-added by the GEMM epilogue into the owners' rows
+    (``aqb_gemm_gate_add_scatter``), and an ``aqb_peer_barrier`` after each.  The video
+    rows' reduce-scatter sums f32 partials at the owner in arrival order, so a run is
+    reproducible to rounding, not bitwise (unlike the Ulysses path).
     """
 
-    def __init__(self, cfg: DiTConfig, sp=None, **kw):
+    def _tp_setup(self, cfg, sp, kw):
         if sp is None or not getattr(sp, "tensor_parallel", False):
-            raise ConfigError("SingleDiTTP needs a TensorSP group", "parallel.tp")
+            raise ConfigError("a TP-SP model needs a TensorSP group", "parallel.tp")
         if kw.get("precision", "bf16") != "bf16":
             raise ConfigError("TP-SP runs the bf16 product path", "model.precision")
         if cfg.head_dim != 128:
             raise ConfigError("TP-SP needs head_dim 128 (fused QK-norm epilogue)", "parallel.tp")
-        super().__init__(cfg, sp=sp, **kw)
-        self.W = tp_shard_single_dit(self.W, cfg, sp.P, sp.rank)
+
+    def _tp_shard(self):
+        self.W = tp_shard(self.W, self.cfg, self.sp.P, self.sp.rank)
         torch.cuda.empty_cache()
 
-    def _prepare_tp(self):
+    def _bind_attention_output(self, i):
+        pass  # TP-SP keeps its own full-sequence, local-head buffers (no attention cache)
+
+    def _rs(self, a, name, gate, flag, run_if, barrier=True):
+        """Row-parallel projection of video rows: this rank's partial reduce-added into the
+        owners' residual rows."""
+        W = self.W
+        ops.gemm_gate_add_scatter(a, W[f"{name}.w"], self.x_dst, self.cfg.hidden_size, self.geo.Sv_loc,
+                                  bias=W[f"{name}.b"], gate=gate, run_flag=flag, run_if=run_if)
+        if barrier:
+            self._barrier(flag, run_if)
+
+    def _ag(self, shift, scale, kind, flag, run_if, probe=False, local=None):
+        """Sequence-parallel LN + modulation (or cast, kind 2) of this rank's video rows into
+        every rank's ``mg``; ``local`` = (shift, scale) of the replicated text rows, normalised
+        in place by each rank (MM-DiT)."""
+        n, H = self.geo.Sv_loc, self.cfg.hidden_size
+        ops.norm_modulate_gather(self.x[:n], shift, scale, self.mg_dst, H, self.cfg.norm_eps, kind=kind,
+                                 probe_prev=self.prev if probe else None,
+                                 probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
+        if local is not None:
+            ops.norm_modulate(self.x[n:], local[0], local[1], self.mg[self.geo.Sv:], self.cfg.norm_eps,
+                              run_flag=flag, run_if=run_if)
+        if probe:
+            self._decide()  # its barrier (carrying the rel-L1 sums) also completes the gather
+        else:
+            self._barrier(flag, run_if)
+
+    def _tp_peer(self, extra: dict):
+        """Symmetric buffers: the gathered modulated input ``mg`` (every rank stores its video
+        rows into every copy) and the residual ``x`` (every rank reduce-adds its partials into
+        the owner's rows), + ``extra``."""
         cfg, g, dev = self.cfg, self.geo, self.device
-        H, D, P = cfg.hidden_size, cfg.head_dim, self.sp.P
+        H = cfg.hidden_size
         self.sp.check(cfg.num_heads, g.Sv, cfg.ffn_dim)
-        hd = self.hl * D
-        S, n = g.Sv, g.Sv_loc
-        # symmetric buffers: the gathered modulated input (every rank stores its rows into
-        # every copy) and the residual (every rank reduce-adds its partials into the owner's rows)
-        self.peer = PeerBuffers(self.sp, {"mg": S * H * 2, "x": n * H * 4, "sig": SIGNAL_BYTES}, dev)
-        self.mg = self.peer.local("mg", (S, H), BF16)
-        self.x = self.peer.local("x", (n, H), F32)
+        S, n, St = g.Sv, g.Sv_loc, g.St
+        sizes = {"mg": (S + St) * H * 2, "x": (n + St) * H * 4, "sig": SIGNAL_BYTES}
+        sizes.update(extra)
+        self.peer = PeerBuffers(self.sp, sizes, dev)
+        self.mg = self.peer.local("mg", (S + St, H), BF16)
+        self.x = self.peer.local("x", (n + St, H), F32)
         self.mg_dst = self.peer.ptrs("mg", self.sp.rank * n * H * 2)
         self.x_dst = self.peer.ptrs("x")
         self.sig = self.peer.ptrs("sig")
         self.epoch = torch.zeros(1, device=dev, dtype=torch.int32)
         self.peer_status = torch.zeros(1, device=dev, dtype=torch.int32)
         e = lambda *s_, dt=BF16: torch.empty(*s_, device=dev, dtype=dt)  # noqa: E731
-        self.qkv_full = e(S, 3 * hd)
-        self.o_full = e(S, hd)
-        self.xq_full = e(S, hd)
-        self.xo_full = e(S, hd)
-        self.h_full = e(S, cfg.ffn_dim // P)
+        hd = self.hl * cfg.head_dim
+        self.qkv_full = e(S + St, 3 * hd)
+        self.o_full = e(S + St, hd)
+        self.h_full = e(S + St, cfg.ffn_dim // self.sp.P)
         self.h = self.h[:0]  # the unsharded buffers are unused under TP
         self.qkv = self.qkv[:0]
+        return e
 
-    def _bind_attention_output(self, i):
-        pass  # TP-SP keeps its own full-sequence, local-head buffers (no attention cache)
 
-    def _rs(self, a, name, gate, flag, run_if):
-        """Row-parallel projection: this rank's partial reduce-added into the owners' residual rows."""
-        W = self.W
-        ops.gemm_gate_add_scatter(a, W[f"{name}.w"], self.x_dst, self.cfg.hidden_size, self.geo.Sv_loc,
-                                  bias=W[f"{name}.b"], gate=gate, run_flag=flag, run_if=run_if)
-        self._barrier(flag, run_if)
+class SingleDiTTP(_TensorParallel, SingleDiT):
+    """Single-DiT under TP-SP.  Per block, six sub-steps each end in a peer barrier:
 
-    def _ag(self, shift, scale, kind, flag, run_if, probe=False):
-        """Sequence-parallel LN + modulation (or cast, kind 2) of this rank's rows into every rank's ``mg``."""
-        ops.norm_modulate_gather(self.x, shift, scale, self.mg_dst, self.cfg.hidden_size, self.cfg.norm_eps,
-                                 kind=kind, probe_prev=self.prev if probe else None,
-                                 probe_partials=self.partials if probe else None, run_flag=flag, run_if=run_if)
-        if probe:
-            self._decide()  # its barrier (carrying the rel-L1 sums) also completes the gather
-        else:
-            self._barrier(flag, run_if)
+      AG(LN+mod(x))  -> QKV(local heads, all rows) -> attention -> proj  -> RS into x
+      AG(bf16 x)     -> q(local heads) -> cross-attention to text -> proj -> RS into x
+      AG(LN+mod(x))  -> FFN1(local columns, GeLU) -> FFN2 -> RS into x
+    """
+
+    def __init__(self, cfg: DiTConfig, sp=None, **kw):
+        self._tp_setup(cfg, sp, kw)
+        super().__init__(cfg, sp=sp, **kw)
+        self._tp_shard()
+
+    def _prepare_tp(self):
+        e = self._tp_peer({})
+        hd = self.hl * self.cfg.head_dim
+        self.xq_full = e(self.geo.Sv, hd)
+        self.xo_full = e(self.geo.Sv, hd)
 
     def _single_dit_block(self, i, flag, run_if, probe, ag):
         cfg, g, W = self.cfg, self.geo, self.W
@@ -759,10 +792,87 @@ class SingleDiTTP(SingleDiT):
         self._rs(self.h_full, f"{p}.fc2", mods[5], flag, run_if)
 
 
+class MMDiTTP(_TensorParallel, MMDiT):
+    """MM-DiT under TP-SP — the paper's own inference layout for the 13.4B model
+    (``PAPER.md:191,197,320``).  Video rows are sequence-sharded as for Single-DiT; the
+    256 text rows are replicated on every rank (their LN runs locally, their
+    row-parallel projections are all-reduced deterministically: gate·partial into every
+    rank's slot, then a rank-ordered sum).  Dual blocks use the per-stream weights on the
+    two row ranges; joint attention runs over video + text rows for the local heads.
+    Per block, four sub-steps each end in a peer barrier (AG → QKV → attention → RS, AG →
+    FFN1 → FFN2 → RS)."""
+
+    def __init__(self, cfg: DiTConfig, sp=None, **kw):
+        self._tp_setup(cfg, sp, kw)
+        super().__init__(cfg, sp=sp, **kw)
+        self._tp_shard()
+
+    def _prepare_tp(self):
+        g, H = self.geo, self.cfg.hidden_size
+        P, St = self.sp.P, g.St
+        e = self._tp_peer({"tslot": P * St * H * 4})
+        self.tslot = self.peer.local("tslot", (P, St, H), F32)
+        self.tslot_dst = self.peer.ptrs("tslot", self.sp.rank * St * H * 4)
+        self.tpart = e(St, H, dt=F32)
+
+    def _text_rs(self, a, name, gate, flag, run_if):
+        """Row-parallel projection of the replicated text rows: f32 partial, gate·partial into
+        this rank's slot on every rank (the barrier follows in the caller)."""
+        W = self.W
+        ops.gemm(a, W[f"{name}.w"], self.tpart, bias=W[f"{name}.b"], epilogue="f32", run_flag=flag, run_if=run_if)
+        ops.gate_bcast(self.tpart, gate, self.tslot_dst, self.cfg.hidden_size, run_flag=flag, run_if=run_if)
+
+    def _tp_block(self, pv, pt, mv, mt, flag, run_if, probe):
+        cfg, g, W = self.cfg, self.geo, self.W
+        D, eps, hl = cfg.head_dim, cfg.qk_norm_eps, self.hl
+        hd = hl * D
+        S, n = g.Sv, g.Sv_loc
+        # joint attention over video + text rows, local heads
+        self._ag(mv[0], mv[1], 0, flag, run_if, probe=probe, local=(mt[0], mt[1]))
+        if pv == pt:
+            ops.gemm_qknorm_rope(self.mg, W[f"{pv}.qkv.w"], self.qkv_full, hd, 2, W[f"{pv}.q_norm"],
+                                 W[f"{pv}.k_norm"], eps, bias=W[f"{pv}.qkv.b"], cos=self.cos, sin=self.sin,
+                                 rope_row0=0, rope_rows=S, run_flag=flag, run_if=run_if)
+        else:
+            ops.gemm_qknorm_rope(self.mg[:S], W[f"{pv}.qkv.w"], self.qkv_full[:S], hd, 2, W[f"{pv}.q_norm"],
+                                 W[f"{pv}.k_norm"], eps, bias=W[f"{pv}.qkv.b"], cos=self.cos, sin=self.sin,
+                                 rope_row0=0, rope_rows=S, run_flag=flag, run_if=run_if)
+            ops.gemm_qknorm_rope(self.mg[S:], W[f"{pt}.qkv.w"], self.qkv_full[S:], hd, 2, W[f"{pt}.q_norm"],
+                                 W[f"{pt}.k_norm"], eps, bias=W[f"{pt}.qkv.b"], run_flag=flag, run_if=run_if)
+        q = self.qkv_full
+        ops.attention(q, q[:, hd:], q[:, 2 * hd:], self.o_full, hl, D, workspace=self.attn_ws, run_flag=flag,
+                      run_if=run_if)
+        self._rs(self.o_full[:S], f"{pv}.proj", mv[2], flag, run_if, barrier=False)
+        self._text_rs(self.o_full[S:], f"{pt}.proj", mt[2], flag, run_if)
+        self._barrier(flag, run_if)
+        ops.sum_slots(self.x[n:], self.tslot, run_flag=flag, run_if=run_if)
+        # MLP
+        self._ag(mv[3], mv[4], 0, flag, run_if, local=(mt[3], mt[4]))
+        if pv == pt:
+            ops.gemm(self.mg, W[f"{pv}.fc1.w"], self.h_full, bias=W[f"{pv}.fc1.b"], epilogue="gelu", run_flag=flag,
+                     run_if=run_if)
+        else:
+            ops.gemm(self.mg[:S], W[f"{pv}.fc1.w"], self.h_full[:S], bias=W[f"{pv}.fc1.b"], epilogue="gelu",
+                     run_flag=flag, run_if=run_if)
+            ops.gemm(self.mg[S:], W[f"{pt}.fc1.w"], self.h_full[S:], bias=W[f"{pt}.fc1.b"], epilogue="gelu",
+                     run_flag=flag, run_if=run_if)
+        self._rs(self.h_full[:S], f"{pv}.fc2", mv[5], flag, run_if, barrier=False)
+        self._text_rs(self.h_full[S:], f"{pt}.fc2", mt[5], flag, run_if)
+        self._barrier(flag, run_if)
+        ops.sum_slots(self.x[n:], self.tslot, run_flag=flag, run_if=run_if)
+
+    def _mm_dual_block(self, i, flag, run_if, probe, ag):
+        pi, pt = f"dual.{i}.img", f"dual.{i}.txt"
+        self._tp_block(pi, pt, self._mod(f"{pi}.mod"), self._mod(f"{pt}.mod"), flag, run_if, probe)
+
+    def _mm_single_block(self, i, flag, run_if, probe, ag):
+        p = f"single.{i}"
+        md = self._mod(f"{p}.mod")
+        self._tp_block(p, p, md, md, flag, run_if, probe)
+
+
 def build_model(cfg: DiTConfig, **kw) -> DiTModel:
     sp = kw.get("sp")
     if sp is not None and getattr(sp, "tensor_parallel", False):
-        if cfg.family != "single-dit":
-            raise ConfigError("TP-SP is implemented for Single-DiT", "parallel.tp")
-        return SingleDiTTP(cfg, **kw)
+        return (SingleDiTTP if cfg.family == "single-dit" else MMDiTTP)(cfg, **kw)
     return (SingleDiT if cfg.family == "single-dit" else MMDiT)(cfg, **kw)

@@ -133,6 +133,23 @@ def norm_modulate_gather(x, shift, scale, outs, ldy, eps=1e-6, kind=0, probe_pre
          int(run_if), _stream())
 
 
+def gate_bcast(src, gate, dsts, ldd, run_flag=None, run_if=1):
+    """gate * src (f32 [rows, cols]) stored into every device address in ``dsts`` (row stride ``ldd``)."""
+    _need(src, F32, "gate_bcast.src")
+    rows, cols = src.shape
+    _run("small", rows * cols * 4 * (1 + len(dsts)), "aqb_gate_bcast", _p(src), src.stride(0), _p(gate),
+         _native.ptr_array(dsts), len(dsts), int(ldd), rows, cols, _p(run_flag), int(run_if), _stream())
+
+
+def sum_slots(x, slots, run_flag=None, run_if=1):
+    """x += sum_k slots[k] in slot order (x f32 [rows, cols], slots f32 [P, rows, cols])."""
+    _need(x, F32, "sum_slots.x")
+    _need(slots, F32, "sum_slots.slots")
+    rows, cols = x.shape
+    _run("small", rows * cols * 4 * (2 + slots.shape[0]), "aqb_sum_slots", _p(x), x.stride(0), _p(slots),
+         slots.shape[0], slots.stride(0), slots.stride(1), rows, cols, _p(run_flag), int(run_if), _stream())
+
+
 def gemm_gate_add_scatter(a, w, peer_out, ldo, rows_per_rank, bias=None, gate=None, run_flag=None, run_if=1):
     """Row-parallel projection partial, gate * (a @ w.T + bias) reduce-added into the residual
     (f32, stride ``ldo``) of the rank owning each row (``peer_out[r]``): the TP-SP reduce-scatter

@@ -107,7 +107,10 @@ class TensorSP(Ulysses):
     GEMM and attention run on the full sequence for the local heads; the row-parallel
     GEMM's epilogue reduce-adds its partial straight into the owning rank's residual
     rows (the reduce-scatter, ``aqb_gemm_gate_add_scatter``).  ``aqb_peer_barrier``
-    orders the steps.  No collective runs on the data path.  Single-DiT only.
+    orders the steps.  No collective runs on the data path.  MM-DiT text rows (replicated on
+    every rank) are all-reduced deterministically: each rank stores gate·partial into its
+    slot of every rank's slot buffer (``aqb_gate_bcast``) and every rank sums the slots in
+    rank order (``aqb_sum_slots``).
     """
 
     tensor_parallel = True
@@ -121,13 +124,33 @@ class TensorSP(Ulysses):
             raise ConfigError(f"ffn_dim {ffn_dim} not divisible into {self.P} x 8-column shards", "parallel.tp")
 
 
-def tp_shard_single_dit(W: dict, cfg, P: int, rank: int) -> dict:
-    """This rank's TP-SP slice of a Single-DiT weight dict (other entries shared, not copied).
+def _tp_rows(t, parts, width, P, rank):
+    """Rows [k*width*P + rank*width, +width) of each of ``parts`` parts (column-parallel slice)."""
+    return torch.cat([t[k * width * P + rank * width:k * width * P + (rank + 1) * width]
+                      for k in range(parts)]).contiguous()
+
+
+def _tp_stream(out: dict, W: dict, p: str, P: int, rank: int, hd: int, fl: int, cross: bool = False):
+    """Slice one attention+MLP stream ``p``: qkv / fc1 (and Single-DiT's xq / xkv) by output
+    rows, proj / fc2 (and xproj) by input columns with the bias on rank 0 only."""
+    col_parallel = [("qkv", 3, hd), ("fc1", 1, fl)] + ([("xq", 1, hd), ("xkv", 2, hd)] if cross else [])
+    row_parallel = [("proj", hd), ("fc2", fl)] + ([("xproj", hd)] if cross else [])
+    for name, parts, width in col_parallel:
+        out[f"{p}.{name}.w"] = _tp_rows(W[f"{p}.{name}.w"], parts, width, P, rank)
+        out[f"{p}.{name}.b"] = _tp_rows(W[f"{p}.{name}.b"], parts, width, P, rank)
+    for name, width in row_parallel:
+        out[f"{p}.{name}.w"] = W[f"{p}.{name}.w"][:, rank * width:(rank + 1) * width].contiguous()
+        out[f"{p}.{name}.b"] = W[f"{p}.{name}.b"] if rank == 0 else None
+
+
+def tp_shard(W: dict, cfg, P: int, rank: int) -> dict:
+    """This rank's TP-SP slice of a weight dict (other entries shared, not copied).
 
     Column-parallel (output rows): ``qkv`` (q, k, v parts: heads [rank*A/P, (rank+1)*A/P)),
-    ``xq``, ``xkv`` (k, v parts), ``fc1`` (hidden columns [rank*F/P, ...)).  Row-parallel
-    (input columns): ``proj``, ``xproj``, ``fc2``; their bias only on rank 0 (``None``
-    elsewhere: the reduce-scatter adds it once)."""
+    ``fc1`` (hidden columns [rank*F/P, ...)), Single-DiT's ``xq`` and ``xkv`` (k, v parts).
+    Row-parallel (input columns): ``proj``, ``fc2``, ``xproj``; their bias only on rank 0
+    (``None`` elsewhere: the reduce adds it once).  MM-DiT: every dual-block stream
+    (``dual.i.img`` / ``dual.i.txt``) and every single block."""
     if cfg.num_heads % P or cfg.ffn_dim % P:
         raise ConfigError(f"heads {cfg.num_heads} / ffn {cfg.ffn_dim} not divisible by {P}", "parallel.tp")
     if not 0 <= rank < P:
@@ -135,20 +158,21 @@ def tp_shard_single_dit(W: dict, cfg, P: int, rank: int) -> dict:
     hd = (cfg.num_heads // P) * cfg.head_dim
     fl = cfg.ffn_dim // P
     out = dict(W)
-
-    def rows(t, parts, width):  # rows [k*width*P + rank*width, +width) of each of `parts` parts
-        return torch.cat([t[k * width * P + rank * width:k * width * P + (rank + 1) * width]
-                          for k in range(parts)]).contiguous()
-
-    for i in range(cfg.num_single):
-        p = f"blocks.{i}"
-        for name, parts, width in (("qkv", 3, hd), ("xq", 1, hd), ("xkv", 2, hd), ("fc1", 1, fl)):
-            out[f"{p}.{name}.w"] = rows(W[f"{p}.{name}.w"], parts, width)
-            out[f"{p}.{name}.b"] = rows(W[f"{p}.{name}.b"], parts, width)
-        for name, width in (("proj", hd), ("xproj", hd), ("fc2", fl)):
-            out[f"{p}.{name}.w"] = W[f"{p}.{name}.w"][:, rank * width:(rank + 1) * width].contiguous()
-            out[f"{p}.{name}.b"] = W[f"{p}.{name}.b"] if rank == 0 else None
+    if cfg.family == "single-dit":
+        for i in range(cfg.num_single):
+            _tp_stream(out, W, f"blocks.{i}", P, rank, hd, fl, cross=True)
+    else:
+        for i in range(cfg.num_dual):
+            for st in ("img", "txt"):
+                _tp_stream(out, W, f"dual.{i}.{st}", P, rank, hd, fl)
+        for i in range(cfg.num_single):
+            _tp_stream(out, W, f"single.{i}", P, rank, hd, fl)
     return out
+
+
+def tp_shard_single_dit(W: dict, cfg, P: int, rank: int) -> dict:
+    """:func:`tp_shard` for a Single-DiT (kept for callers of the first TP-SP release)."""
+    return tp_shard(W, cfg, P, rank)
 
 
 def oversubscribed() -> bool:

@@ -1,5 +1,5 @@
 #!/usr/bin/env python
-"""Multi-GPU TP-SP parity: P-rank tensor-parallel Single-DiT denoise vs 1 GPU and the CPU oracle.
+"""Multi-GPU TP-SP parity: P-rank tensor-parallel Single-DiT and MM-DiT denoise vs 1 GPU and the CPU oracle.
 
     torchrun --nproc-per-node P --master-addr 127.0.0.1 scripts/tp_check.py
     AQB_OVERSUBSCRIBE=1 torchrun --nproc-per-node 8 ... (P=8 on fewer GPUs)
@@ -38,19 +38,24 @@ def main():
          (3, 8, 16)),
         ("single-16h", DiTConfig("single-dit", hidden_size=2048, num_heads=16, num_single=2, text_dim=256,
                                  text_len=40), (5, 8, 24)),
+        ("mm", DiTConfig("mm-dit", hidden_size=1024, num_heads=8, num_dual=2, num_single=2, text_dim=192, text_len=24,
+                         pooled_dim=64), (2, 8, 16)),
+        ("mm-24h", DiTConfig("mm-dit", hidden_size=3072, num_heads=24, num_dual=1, num_single=1, text_dim=192,
+                             text_len=24, pooled_dim=64), (2, 8, 16)),
     ]
     for name, cfg, grid in cases:
         W = init_weights(cfg, seed=0)
         inp = synthetic_inputs(cfg, grid)
-        m_tp = build_model(cfg, weights=W, sp=sp).prepare(grid, inp["text"])
+        pooled = inp["pooled"] if cfg.family == "mm-dit" else None
+        m_tp = build_model(cfg, weights=W, sp=sp).prepare(grid, inp["text"], pooled)
         for cache in (plan_cache(8, warmup=2, interval=2), RelL1Policy(threshold=0.06, warmup=2)):
             r_tp = denoise(m_tp, inp["x0"], 8, cache, trajectory=True)
             good = m_tp.peer_ok()
             if sp.rank == 0:
-                m1 = build_model(cfg, weights=W).prepare(grid, inp["text"])
+                m1 = build_model(cfg, weights=W).prepare(grid, inp["text"], pooled)
                 r1 = denoise(m1, inp["x0"], 8, cache, trajectory=True)
-                orc = ref.OracleDiT(cfg, W, inp["text"], None, grid, n_front=front_block_count(cfg.num_layers, 0.25),
-                                    mode=cache.mode)
+                orc = ref.OracleDiT(cfg, W, inp["text"], pooled, grid,
+                                    n_front=front_block_count(cfg.num_layers, 0.25), mode=cache.mode)
                 if isinstance(cache, RelL1Policy):
                     lat, taken, _ = ref.denoise(orc, inp["x0"], 8, policy=cache)
                 else:

@@ -225,7 +225,8 @@ def test_temporal_multidiffusion_matches_oracle(name, n_prime, window, stride):
     assert max(errs) <= TOL_BF16, errs
 
 
-def test_tp_sp_single_rank_matches_plain_model_and_oracle():
+@pytest.mark.parametrize("family", ["single-dit", "mm-dit"])
+def test_tp_sp_single_rank_matches_plain_model_and_oracle(family):
     """TP-SP code path (fused gather / reduce-scatter kernels, peer barriers) with P = 1 in this
     process (gloo group of one): same schedule as the plain model, within bf16 noise of it and of
     the oracle.  Multi-rank parity: scripts/tp_check.py."""
@@ -242,13 +243,19 @@ def test_tp_sp_single_rank_matches_plain_model_and_oracle():
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=0, world_size=1)
     try:
-        cfg = DiTConfig("single-dit", hidden_size=1024, num_heads=8, num_single=4, text_dim=256, text_len=40)
-        grid = (3, 8, 16)
+        if family == "single-dit":
+            cfg = DiTConfig("single-dit", hidden_size=1024, num_heads=8, num_single=4, text_dim=256, text_len=40)
+            grid = (3, 8, 16)
+        else:
+            cfg = DiTConfig("mm-dit", hidden_size=1024, num_heads=8, num_dual=2, num_single=2, text_dim=192,
+                            text_len=24, pooled_dim=64)
+            grid = (2, 8, 16)
         W = init_weights(cfg, seed=0)
         inp = synthetic_inputs(cfg, grid)
-        tp = build_model(cfg, weights=W, sp=TensorSP()).prepare(grid, inp["text"])
-        plain = build_model(cfg, weights=W).prepare(grid, inp["text"])
-        orc = ref.OracleDiT(cfg, W, inp["text"], None, grid, n_front=front_block_count(cfg.num_layers, 0.25))
+        pooled = inp["pooled"] if family == "mm-dit" else None
+        tp = build_model(cfg, weights=W, sp=TensorSP()).prepare(grid, inp["text"], pooled)
+        plain = build_model(cfg, weights=W).prepare(grid, inp["text"], pooled)
+        orc = ref.OracleDiT(cfg, W, inp["text"], pooled, grid, n_front=front_block_count(cfg.num_layers, 0.25))
         for cache in (plan_cache(8, warmup=2, interval=2), RelL1Policy(threshold=0.06, warmup=2)):
             r_tp = denoise(tp, inp["x0"], 8, cache, trajectory=True)
             r_1 = denoise(plain, inp["x0"], 8, cache, trajectory=True)
