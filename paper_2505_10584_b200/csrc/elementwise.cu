@@ -137,7 +137,7 @@ AQB_DEV float block_sum(float v, float* red) {
   return t;
 }
 
-template <int NW, typename OutT>
+template <int NW, int VPT, typename OutT>
 __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __restrict__ x, int64_t ldx,
                                                                const float* __restrict__ shift,
                                                                const float* __restrict__ scale, const Outs<OutT> ys,
@@ -148,25 +148,55 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
   pdl_trigger();
   if (!gate_open(flag, run_if)) return;
   __shared__ float red[NW];
-  constexpr int T = NW * 32, H = T * 16;
+  constexpr int T = NW * 32, H = T * 4 * VPT;
   const int64_t row = blockIdx.x;
   const int tid = threadIdx.x;
   const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
-  float4 v[4];
+  float4 v[VPT];
 #pragma unroll
-  for (int j = 0; j < 4; ++j) v[j] = ld_stream(xr + tid + T * j);
+  for (int j = 0; j < VPT; ++j) v[j] = ld_stream(xr + tid + T * j);
   float mean = 0.f;
-  if (kind == 0) {
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
-    mean = block_sum<NW>(s, red) * (1.f / H);
-  }
   float rstd = 1.f;
-  if (kind != 2) {
+  if (kind == 0) {
+    // mean and variance in ONE block round: per-thread (mean, M2) over its 16 values,
+    // merged pairwise (Chan et al., equal counts) through the warp and then the NW warps
+    float m = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) m += (v[j].x + v[j].y) + (v[j].z + v[j].w);
+    m *= 1.f / (4 * VPT);
+    float m2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) {
+      const float a = v[j].x - m, b = v[j].y - m, c = v[j].z - m, d = v[j].w - m;
+      m2 += (a * a + b * b) + (c * c + d * d);
+    }
+    float n = 4.f * VPT;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const float mo = __shfl_xor_sync(0xffffffffu, m, o), m2o = __shfl_xor_sync(0xffffffffu, m2, o);
+      const float d = mo - m;
+      m2 = m2 + m2o + d * d * (0.5f * n);
+      m = 0.5f * (m + mo);
+      n *= 2.f;
+    }
+    __shared__ float2 wstat[NW];
+    if ((tid & 31) == 0) wstat[tid >> 5] = make_float2(m, m2);
+    __syncthreads();
+    constexpr float kW = 128.f * VPT;  // values per warp
+    float bm = wstat[0].x, bm2 = wstat[0].y, bn = kW;
+#pragma unroll
+    for (int w = 1; w < NW; ++w) {
+      const float d = wstat[w].x - bm, nn = bn + kW;
+      bm += d * (kW / nn);
+      bm2 += wstat[w].y + d * d * (bn * kW / nn);
+      bn = nn;
+    }
+    mean = bm;
+    rstd = rsqrtf(bm2 * (1.f / H) + eps);
+  } else if (kind == 1) {
     float ss = 0.f;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < VPT; ++j) {
       const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
       ss += (a * a + b * b) + (c * c + d * d);
     }
@@ -178,7 +208,7 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
   float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
   float dsum = 0.f, psum = 0.f;
 #pragma unroll
-  for (int j = 0; j < 4; ++j) {
+  for (int j = 0; j < VPT; ++j) {
     const int c4 = tid + T * j;
     const float4 sc = scale ? __ldg(sc4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 sh = shift ? __ldg(sh4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
@@ -547,19 +577,36 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
   if (rows <= 0) return AQB_OK;
   const int grid = static_cast<int>((rows + 7) / 8);
   cudaStream_t s = reinterpret_cast<cudaStream_t>(stream);
-  if (hidden >= 1024 && hidden % 512 == 0) {  // CTA per row (hidden/16 threads)
-    switch (hidden / 512) {
-#define NMR_CASE(NW)                                                                                               \
-  case NW:                                                                                                         \
-    AQB_CUDA_TRY(launch_pdl(norm_mod_row_kernel<NW, OutT>, dim3(unsigned(rows)), dim3(NW * 32), 0, s, x, ldx, shift, scale, yb, ldy, rows, eps,     \
-                                                                     norm_kind, probe_prev, probe_partials,        \
-                                                                     run_flag, run_if));                            \
-    AQB_LAUNCH_CHECK();                                                                                            \
-    return AQB_OK;
-      NMR_CASE(2) NMR_CASE(3) NMR_CASE(4) NMR_CASE(5) NMR_CASE(6) NMR_CASE(7) NMR_CASE(8)
-#undef NMR_CASE
-      default: break;
+  // CTA per row for wide rows: NW warps x VPT float4 per thread.  Measured (B200, L2
+  // flushed): hidden 2048 VPT 4 (4 warps) 3.34 TB/s vs 2.60 / 2.92 for VPT 2 / 8;
+  // hidden 3072 VPT 8 (3 warps) 4.69 TB/s vs 4.12 for VPT 4.  AQB_NORM_VPT = 2|4|8 forces.
+  static int vpt_env = -1;
+  if (vpt_env < 0) {
+    const char* e = getenv("AQB_NORM_VPT");
+    vpt_env = e ? atoi(e) : 0;
+    if (vpt_env != 2 && vpt_env != 4 && vpt_env != 8) vpt_env = 0;
+  }
+  const int vpt = vpt_env ? vpt_env : (hidden >= 3072 && hidden % 1024 == 0 ? 8 : 4);
+  if (hidden >= 1024 && hidden % (128 * vpt) == 0 && hidden / (128 * vpt) >= 2 && hidden / (128 * vpt) <= 16) {
+    const int nw = hidden / (128 * vpt);
+#define NMR_LAUNCH(NW, VPT)                                                                                      \
+  AQB_CUDA_TRY(launch_pdl(norm_mod_row_kernel<NW, VPT, OutT>, dim3(unsigned(rows)), dim3(NW * 32), 0, s, x, ldx,  \
+                          shift, scale, yb, ldy, rows, eps, norm_kind, probe_prev, probe_partials, run_flag,     \
+                          run_if));                                                                              \
+  AQB_LAUNCH_CHECK();                                                                                            \
+  return AQB_OK;
+#define NMR_CASE(NW, VPT) \
+  case NW:                \
+    NMR_LAUNCH(NW, VPT)
+    if (vpt == 4) {
+      switch (nw) { NMR_CASE(2, 4) NMR_CASE(3, 4) NMR_CASE(4, 4) NMR_CASE(5, 4) NMR_CASE(6, 4) NMR_CASE(7, 4) NMR_CASE(8, 4) default: break; }
+    } else if (vpt == 2) {
+      switch (nw) { NMR_CASE(4, 2) NMR_CASE(6, 2) NMR_CASE(8, 2) NMR_CASE(12, 2) NMR_CASE(16, 2) default: break; }
+    } else {
+      switch (nw) { NMR_CASE(2, 8) NMR_CASE(3, 8) NMR_CASE(4, 8) default: break; }
     }
+#undef NMR_CASE
+#undef NMR_LAUNCH
   }
 #define NM_CASE(NV)                                                                                          \
   case NV:                                                                                                   \
