@@ -466,3 +466,29 @@ def test_gemm_gate_add_scatter_reduces_into_row_owners(rpr, n, k):
         exp += gate * (a.float() @ w.float().t() + (b if b is not None else 0))
         ops.gemm_gate_add_scatter(a, w, [r.data_ptr() for r in res], n, rpr, bias=b, gate=gate)
     assert rel_l2(torch.cat(res), exp) < 1e-5
+
+
+def test_gate_bcast_and_rank_ordered_slot_sum():
+    """MM-DiT TP-SP text-row all-reduce: gate*partial into every rank's slot, then x += slots in
+    rank order (bitwise the same sum on every rank)."""
+    P, rows, cols = 3, 24, 512
+    g = torch.Generator(device=dev).manual_seed(11)
+    parts = [torch.randn(rows, cols, device=dev, generator=g) for _ in range(P)]
+    gate = torch.randn(cols, device=dev, generator=g)
+    slots = [torch.zeros(P, rows, cols, device=dev) for _ in range(P)]  # one slot buffer per "rank"
+    for r in range(P):  # rank r writes its slot r on every rank
+        ops.gate_bcast(parts[r], gate, [s[r].data_ptr() for s in slots], cols)
+    x0 = torch.randn(rows, cols, device=dev, generator=g)
+    xs = [x0.clone() for _ in range(P)]
+    for r in range(P):
+        ops.sum_slots(xs[r], slots[r])
+    exp = x0.clone()
+    for r in range(P):
+        exp = exp + gate * parts[r]
+    for r in range(P):
+        assert torch.equal(xs[r], xs[0])  # replicated rows stay identical
+    assert rel_l2(xs[0], exp) < 1e-6
+    flag = torch.zeros(1, device=dev, dtype=torch.int32)  # gated off: untouched
+    y = x0.clone()
+    ops.sum_slots(y, slots[0], run_flag=flag, run_if=1)
+    assert torch.equal(y, x0)

@@ -125,3 +125,36 @@ def test_window_average_kernel(n_prime, n, s, hw):
     for i in range(n_prime):
         cov = [vals[k] for k, (a, b) in enumerate(plan.clips) if a <= i < b]
         assert torch.allclose(out[:, i], torch.full_like(out[:, i], sum(cov) / len(cov)))
+
+
+@pytest.mark.gpu
+def test_peer_tiles_single_rank_blend_equals_local_blend():
+    """PeerTiles (multi-GPU VAE blend) with a group of one: tiles written into the peer buffer
+    blend to the same bits as the plain blend of the same tiles (scripts/vae_blend_check.py: P=2)."""
+    import socket
+
+    import torch.distributed as dist
+
+    from paper_2505_10584_b200.parallel import Ulysses
+    from paper_2505_10584_b200.tiling import PeerTiles
+
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        plan = plan_vae_tiles((9, 40, 64), (5, 16, 24), (1, 4, 8), devices=1)
+        g = torch.Generator().manual_seed(1)
+        tiles = [torch.randn(4, *t.size, generator=g) for t in plan.tiles]
+        pt = PeerTiles(plan, Ulysses(exchange="p2p"), 4)
+        for i in plan.tiles_of(0):
+            pt.local_tile(i).copy_(tiles[i])
+        out = torch.empty(4, *plan.latent, device="cuda")
+        ref = torch.empty_like(out)
+        pt.blend(out)
+        blend_tiles(plan, [t.cuda() for t in tiles], ref)
+        assert torch.equal(out, ref)
+        pt.close()
+    finally:
+        dist.destroy_process_group()
