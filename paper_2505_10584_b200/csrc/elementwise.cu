@@ -6,6 +6,7 @@
 // Design rules (blackwell guide G2/G7/G13): thread->contiguous element,
 // 16-byte vector loads/stores, warp-shuffle reductions, one warp per row
 // so the whole row lives in registers (single HBM read), fp32 statistics.
+#include <algorithm>
 #include <cmath>
 
 #include "host.cuh"
@@ -149,12 +150,22 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
   if (!gate_open(flag, run_if)) return;
   __shared__ float red[NW];
   constexpr int T = NW * 32, H = T * 4 * VPT;
-  const int64_t row = blockIdx.x;
   const int tid = threadIdx.x;
-  const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
-  float4 v[VPT];
+  // persistent over rows (grid-stride) with the next row's loads issued before this row's
+  // reductions, so each CTA keeps two rows in flight
+  float4 v[VPT], vn[VPT];
+  int64_t row = blockIdx.x;
+  if (row < rows) {
+    const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
 #pragma unroll
-  for (int j = 0; j < VPT; ++j) v[j] = ld_stream(xr + tid + T * j);
+    for (int j = 0; j < VPT; ++j) v[j] = ld_stream(xr + tid + T * j);
+  }
+  for (; row < rows; row += gridDim.x) {
+  if (row + gridDim.x < rows) {
+    const float4* xn = reinterpret_cast<const float4*>(x + (row + gridDim.x) * ldx);
+#pragma unroll
+    for (int j = 0; j < VPT; ++j) vn[j] = ld_stream(xn + tid + T * j);
+  }
   float mean = 0.f;
   float rstd = 1.f;
   if (kind == 0) {
@@ -233,6 +244,10 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
       partials[row] = dsum;
       partials[rows + row] = psum;
     }
+  }
+  __syncthreads();  // wstat / red reused by the next row
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) v[j] = vn[j];
   }
 }
 
@@ -589,8 +604,19 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
   const int vpt = vpt_env ? vpt_env : (hidden >= 3072 && hidden % 1024 == 0 ? 8 : 4);
   if (hidden >= 1024 && hidden % (128 * vpt) == 0 && hidden / (128 * vpt) >= 2 && hidden / (128 * vpt) <= 16) {
     const int nw = hidden / (128 * vpt);
+    // persistent CTAs per SM (AQB_NORM_CTAS_PER_SM overrides).  Measured: hidden 2048
+    // (VPT 4) 8 per SM 3.74 TB/s vs 3.34 with a CTA per row; hidden 3072 (VPT 8) 4 per SM.
+    static int cps_env = -1;
+    if (cps_env < 0) {
+      const char* e = getenv("AQB_NORM_CTAS_PER_SM");
+      cps_env = e ? atoi(e) : 0;
+      if (cps_env < 0) cps_env = 0;
+    }
+    const int cps = cps_env ? cps_env : (vpt == 8 ? 4 : 8);
+    const int64_t row_grid = int64_t(sm_count()) * cps;
 #define NMR_LAUNCH(NW, VPT)                                                                                      \
-  AQB_CUDA_TRY(launch_pdl(norm_mod_row_kernel<NW, VPT, OutT>, dim3(unsigned(rows)), dim3(NW * 32), 0, s, x, ldx,  \
+  AQB_CUDA_TRY(launch_pdl(norm_mod_row_kernel<NW, VPT, OutT>, dim3(unsigned(std::min<int64_t>(rows, row_grid))),    \
+                          dim3(NW * 32), 0, s, x, ldx,                                                           \
                           shift, scale, yb, ldy, rows, eps, norm_kind, probe_prev, probe_partials, run_flag,     \
                           run_if));                                                                              \
   AQB_LAUNCH_CHECK();                                                                                            \
