@@ -182,6 +182,10 @@ int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t h
 /* tiles (head x 256 queries) the automatic plan runs in one pass; the rest split
  * aqb_attention_splits ways (wave-quantisation tail, or all tiles when few) */
 int aqb_attention_whole_tiles(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
+/* 256-query blocks of one head each CTA of a one-pass launch runs with K/V loaded
+ * once (short KV: 2 x KV blocks fit the K/V ring, e.g. cross-attention to 256 text
+ * tokens); 1 = one block per CTA.  AQB_ATTN_PAIRS=g in the environment forces g. */
+int aqb_attention_pairs_per_cta(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
 /* workspace for any plan of <= kv_splits splits, and for the automatic plan */
 int64_t aqb_attention_workspace_bytes(int64_t seq_q, int32_t heads, int32_t head_dim, int32_t kv_splits);
 int64_t aqb_attention_auto_workspace_bytes(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);

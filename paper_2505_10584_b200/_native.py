@@ -42,6 +42,7 @@ SIGNATURES = {
     "aqb_attention_splits": (c_int, [c_int64, c_int64, c_int32, c_int32]),
     "aqb_attention_workspace_bytes": (c_int64, [c_int64, c_int32, c_int32, c_int32]),
     "aqb_attention_whole_tiles": (c_int, [c_int64, c_int64, c_int32, c_int32]),
+    "aqb_attention_pairs_per_cta": (c_int, [c_int64, c_int64, c_int32, c_int32]),
     "aqb_attention_auto_workspace_bytes": (c_int64, [c_int64, c_int64, c_int32, c_int32]),
     "aqb_attention_fwd_scatter": (c_int, [P, c_int64, c_int64, P, c_int64, c_int64, P, c_int64, c_int64, P, c_int32,
                                           c_int64, c_int64, c_int64, c_int64, c_int64, c_int64, c_int32, c_int32,

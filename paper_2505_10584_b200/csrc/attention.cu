@@ -43,8 +43,8 @@ constexpr int BKV = 128;  // keys per KV tile (MMA N of QK^T, K of PV)
 constexpr int kThreads = 384;    // 3 warpgroups: control | softmax tile 0 | softmax tile 1
 constexpr uint32_t kCtrlRegs = 56;     // setmaxnreg budgets: 56 + 2 * 224 <= 512 per SMSP
 constexpr uint32_t kSoftmaxRegs = 224;
-constexpr uint32_t kPolyMaskDefault = 0x52;
-constexpr uint32_t kPCol = 64;         // P_t (bf16 pairs) lives in columns 64..127 of S_t   // pairs (i & 7) in {1,4,6}: exp2 by polynomial (3/8 off the MUFU)
+constexpr uint32_t kPolyMaskDefault = 0x52;  // pairs (i & 7) in {1,4,6}: exp2 by polynomial (3/8 off the MUFU)
+constexpr uint32_t kPCol = 64;               // P_t (bf16 pairs) lives in columns 64..127 of S_t
 
 template <int D>
 struct Cfg {
@@ -95,6 +95,13 @@ struct Params {
   // opart/lse in compact order ((tile - n_whole) * splits + split) * 256 + row.
   int q_pairs, n_whole;
   int splits, kv_blocks_per_split;
+  // Short KV (2 * KV blocks <= ring depth, e.g. cross-attention to 256 text tokens):
+  // a whole CTA runs `pairs_per_cta` consecutive 256-query blocks of one head with
+  // K/V loaded once and resident, so the per-CTA fixed cost (prologue, K/V load,
+  // pipeline fill) is paid once per pairs_per_cta blocks.  CTA c: head c / cpb,
+  // blocks [(c % cpb) * pairs_per_cta, +pairs_per_cta), cpb = ceil(q_pairs / ppc).
+  // 1 = one block per CTA (the tile plan above).
+  int pairs_per_cta;
   float* opart;                     // [tail tiles][splits][256][part_d] f32 (O / l of the split)
   float* lse;                       // [tail tiles][splits][256] f32, log2-sum-exp2 of the split
   int part_d;                       // row stride of opart (the kernel's D)
@@ -128,8 +135,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint8_t* sQ = base + C::kOffQ;
   uint8_t* sKV = base + C::kOffKV;
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::kOffBar);
-  uint64_t* q_full = bars;              // 1
-  uint64_t* kv_full = bars + 1;         // NS
+  uint64_t* q_full = bars;              // 2 (per Q tile)
+  uint64_t* q_empty = bars + 2;         // 2 (last QK^T of a block done: Q buffer free)
+  uint64_t* kv_full = bars + 4;         // NS
   uint64_t* kv_empty = kv_full + C::NS; // NS
   uint64_t* s_full = kv_empty + C::NS;  // 2
   uint64_t* p_full = s_full + 2;        // 2
@@ -139,19 +147,27 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_idx(), lane = lane_idx();
   const int cta = blockIdx.x;
   const bool whole = cta < p.n_whole;
-  const int tile = whole ? cta : p.n_whole + (cta - p.n_whole) / p.splits;
+  const int ppc = p.pairs_per_cta;
+  const int cpb = (p.q_pairs + ppc - 1) / ppc;  // CTAs per head (multi-block mode)
+  const int tile = whole ? (ppc > 1 ? (cta / cpb) * p.q_pairs + (cta % cpb) * ppc : cta)
+                         : p.n_whole + (cta - p.n_whole) / p.splits;
   const int split = whole ? 0 : (cta - p.n_whole) % p.splits;
   const int head = tile / p.q_pairs;
-  const int q0 = (tile % p.q_pairs) * (2 * BQ);
+  const int pair0 = tile % p.q_pairs;                        // first 256-query block
+  const int npair = ppc > 1 ? min(ppc, p.q_pairs - pair0) : 1;
   const int nkv_all = (p.seq_kv + BKV - 1) / BKV;
   const int j0 = whole ? 0 : split * p.kv_blocks_per_split;  // first KV block of this CTA
   const int nkv = whole ? nkv_all : min(nkv_all - j0, p.kv_blocks_per_split);
+  const int nblk = npair * nkv;                              // flattened (block, KV block) steps
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tq);
     tma_prefetch_desc(&tk);
     tma_prefetch_desc(&tv);
-    mbar_init(q_full, 1);
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(q_full + t, 1);
+      mbar_init(q_empty + t, 1);
+    }
     for (int s = 0; s < C::NS; ++s) {
       mbar_init(kv_full + s, 1);
       mbar_init(kv_empty + s, 1);
@@ -177,11 +193,15 @@ __global__ void __launch_bounds__(kThreads, 1)
     // ------------------------------------------------------------ producer
     setmaxnreg_dec<kCtrlRegs>();
     // warp-wide loop, one elected lane per TMA op (keeps operands in uniform registers)
-    if (elect_one()) mbar_arrive_expect_tx(q_full, 2 * C::kQBytes);
-    for (int t = 0; t < 2; ++t)
+    auto load_q = [&](int t, int kk) {
+      if (elect_one()) mbar_arrive_expect_tx(q_full + t, C::kQBytes);
       for (int c = 0; c < C::kBoxes; ++c)
         if (elect_one())
-          tma_load_3d(sQ + t * C::kQBytes + c * (BQ * 128), &tq, q_full, c * 64, head, q0 + t * BQ, kEvictFirst);
+          tma_load_3d(sQ + t * C::kQBytes + c * (BQ * 128), &tq, q_full + t, c * 64, head,
+                      (pair0 + kk) * (2 * BQ) + t * BQ, kEvictFirst);
+    };
+    load_q(0, 0);
+    load_q(1, 0);
     for (int i = 0; i < 2 * nkv; ++i) {
       const int s = i % C::NS;
       const uint32_t ph = (i / C::NS) & 1;
@@ -193,6 +213,12 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (elect_one())
           tma_load_3d(sKV + s * C::kKVBytes + c * (BKV * 128), m, kv_full + s, c * 64, head, row, kEvictLast);
     }
+    // later blocks (K/V stay resident): tile t's next Q as soon as its last QK^T has read Q_t
+    for (int kk = 1; kk < npair; ++kk)
+      for (int t = 0; t < 2; ++t) {
+        mbar_wait(q_empty + t, (kk - 1) & 1);
+        load_q(t, kk);
+      }
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs the loop (all values warp-uniform) and one elected lane
@@ -227,35 +253,48 @@ __global__ void __launch_bounds__(kThreads, 1)
       auto commit = [&](uint64_t* bar) {
         if (elect_one()) umma_commit(bar);
       };
-      mbar_wait(q_full, 0);
-      tc_fence_after();
-      for (int j = 0; j <= nkv; ++j) {
-        const int ik = 2 * j, iv = 2 * (j - 1) + 1;  // ring indices of K_j and V_{j-1}
-        if (j < nkv) {
+      // Flattened over (256-query block kk, KV block j): step J = kk * nkv + j issues
+      // PV of step J-1 and QK^T of step J for both tiles.  At a block boundary both
+      // PVs go first (tile 1's epilogue must not wait behind tile 0's Q reload).
+      for (int J = 0; J <= nblk; ++J) {
+        const int j = J % nkv, kk = J / nkv, jp = (J + nkv - 1) % nkv;
+        const int ik = 2 * j, iv = 2 * jp + 1;  // ring indices of K_j and V_{jp} (resident when npair > 1)
+        const bool qk = J < nblk, pv = J > 0, first = qk && j == 0;
+        if (qk) {
           mbar_wait(kv_full + ik % C::NS, (ik / C::NS) & 1);
           tc_fence_after();
         }
-        if (j > 0) {
+        auto do_pv = [&](int t) {
+          mbar_wait(p_full + t, (J - 1) & 1);
+          tc_fence_after();
+          issue_pv(t, iv % C::NS, jp > 0);
+          commit(o_ready + t);
+        };
+        auto do_qk = [&](int t) {
+          if (first) {
+            mbar_wait(q_full + t, kk & 1);
+            tc_fence_after();
+          }
+          issue_qk(t, ik % C::NS);
+          commit(s_full + t);
+          if (j == nkv - 1 && kk + 1 < npair) commit(q_empty + t);  // Q_t read: the next block's Q may land
+        };
+        if (pv) {
           mbar_wait(kv_full + iv % C::NS, (iv / C::NS) & 1);
-          mbar_wait(p_full + 0, (j - 1) & 1);
           tc_fence_after();
-          issue_pv(0, iv % C::NS, j > 1);
-          commit(o_ready + 0);
+          do_pv(0);
+          if (first) {
+            do_pv(1);
+            commit(kv_empty + iv % C::NS);
+          }
         }
-        if (j < nkv) {
-          issue_qk(0, ik % C::NS);
-          commit(s_full + 0);
-        }
-        if (j > 0) {
-          mbar_wait(p_full + 1, (j - 1) & 1);
-          tc_fence_after();
-          issue_pv(1, iv % C::NS, j > 1);
-          commit(o_ready + 1);
+        if (qk) do_qk(0);
+        if (pv && !first) {
+          do_pv(1);
           commit(kv_empty + iv % C::NS);
         }
-        if (j < nkv) {
-          issue_qk(1, ik % C::NS);
-          commit(s_full + 1);
+        if (qk) {
+          do_qk(1);
           commit(kv_empty + ik % C::NS);
         }
       }
@@ -275,180 +314,187 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint64_t kM = f2pack(12582912.f, 12582912.f);  // 1.5 * 2^23: round-to-nearest
     const uint64_t kC0 = f2pack(0.99992806f, 0.99992806f), kC1 = f2pack(0.69326103f, 0.69326103f);
     const uint64_t kC2 = f2pack(0.24261117f, 0.24261117f), kC3 = f2pack(0.05517162f, 0.05517162f);
-    float m_run = -INFINITY, l_run = 0.f;     // m_run in raw score units
+    for (int kk = 0; kk < npair; ++kk) {
+      const int q0 = (pair0 + kk) * (2 * BQ);
+      float m_run = -INFINITY, l_run = 0.f;     // m_run in raw score units
 
-    for (int j = 0; j < nkv; ++j) {
-      mbar_wait(s_full + t, j & 1);
-      tc_fence_after();
-      uint32_t sr[BKV];
-      tmem_ld64(s_tmem, sr);
-      tmem_ld64(s_tmem + 64, sr + 64);
-      tmem_wait_ld();
-      const int kv_valid = p.seq_kv - (j0 + j) * BKV;
-      if (kv_valid < BKV) {
-#pragma unroll
-        for (int i = 0; i < BKV; ++i)
-          if (i >= kv_valid) sr[i] = 0xff800000u;  // -inf
-      }
-      // row max as 8 independent FMNMX3 chains + a 3-level tree (a single 64-long
-      // dependent chain was the softmax's critical path)
-      float mm[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) mm[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
-#pragma unroll
-      for (int i = 16; i < BKV; i += 16)
-#pragma unroll
-        for (int k = 0; k < 8; ++k)
-          mm[k] = fmaxf(mm[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
-      const float mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
-                             fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
-      // PV_{j-1} must be done before O is rescaled or P_t overwritten.
-      if (j > 0) {
-        mbar_wait(o_ready + t, (j - 1) & 1);
+      for (int j = 0; j < nkv; ++j) {
+        const int J = kk * nkv + j;
+        mbar_wait(s_full + t, J & 1);
         tc_fence_after();
-      }
-      // lazy rescale: only when the running max grows by more than 2^8 in exp2 units
-      const bool need = (mx - m_run) * c > 8.f;
-      if (__any_sync(0xffffffffu, need)) {
-        const float m_new = need ? mx : m_run;
-        const float alpha = need ? ex2((m_run - m_new) * c) : 1.f;
+        uint32_t sr[BKV];
+        tmem_ld64(s_tmem, sr);
+        tmem_ld64(s_tmem + 64, sr + 64);
+        tmem_wait_ld();
+        const int kv_valid = p.seq_kv - (j0 + j) * BKV;
+        if (kv_valid < BKV) {
+#pragma unroll
+          for (int i = 0; i < BKV; ++i)
+            if (i >= kv_valid) sr[i] = 0xff800000u;  // -inf
+        }
+        // row max as 8 independent FMNMX3 chains + a 3-level tree (a single 64-long
+        // dependent chain was the softmax's critical path)
+        float mm[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mm[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
+#pragma unroll
+        for (int i = 16; i < BKV; i += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            mm[k] = fmaxf(mm[k], fmaxf(__uint_as_float(sr[i + k]), __uint_as_float(sr[i + 8 + k])));
+        const float mx = fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
+                               fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7])));
+        // PV_{j-1} must be done before O is rescaled or P_t overwritten.
         if (j > 0) {
+          mbar_wait(o_ready + t, (J - 1) & 1);
+          tc_fence_after();
+        }
+        // lazy rescale: only when the running max grows by more than 2^8 in exp2 units
+        const bool need = (mx - m_run) * c > 8.f;
+        if (__any_sync(0xffffffffu, need)) {
+          const float m_new = need ? mx : m_run;
+          const float alpha = need ? ex2((m_run - m_new) * c) : 1.f;
+          if (j > 0) {
 #pragma unroll 1
-          for (int cc = 0; cc < D / 32; ++cc) {
-            uint32_t u[32];
-            tmem_ld32(o_tmem + cc * 32, u);
-            tmem_wait_ld();
+            for (int cc = 0; cc < D / 32; ++cc) {
+              uint32_t u[32];
+              tmem_ld32(o_tmem + cc * 32, u);
+              tmem_wait_ld();
 #pragma unroll
-            for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
-            tmem_st32(o_tmem + cc * 32, u);
+              for (int i = 0; i < 32; ++i) u[i] = __float_as_uint(__uint_as_float(u[i]) * alpha);
+              tmem_st32(o_tmem + cc * 32, u);
+            }
+            tmem_wait_st();
           }
-          tmem_wait_st();
+          l_run *= alpha;
+          m_run = m_new;
         }
-        l_run *= alpha;
-        m_run = m_new;
-      }
-      const float nm = -m_run * c;
-      const uint64_t nm2 = f2pack(nm, nm);
-      uint64_t acc2[4];  // 4 independent packed row-sum chains
+        const float nm = -m_run * c;
+        const uint64_t nm2 = f2pack(nm, nm);
+        uint64_t acc2[4];  // 4 independent packed row-sum chains
 #pragma unroll
-      for (int q = 0; q < 4; ++q) acc2[q] = f2pack(0.f, 0.f);
-      uint32_t pp[16];  // 16 packed bf16 pairs = 16 TMEM columns, stored as they fill
+        for (int q = 0; q < 4; ++q) acc2[q] = f2pack(0.f, 0.f);
+        uint32_t pp[16];  // 16 packed bf16 pairs = 16 TMEM columns, stored as they fill
 #pragma unroll
-      for (int kc = 0; kc < BKV / 8; ++kc) {
+        for (int kc = 0; kc < BKV / 8; ++kc) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int pi = kc * 4 + q;
-          const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * pi]), __uint_as_float(sr[2 * pi + 1])), c2, nm2);
-          float x0, x1, p0, p1;
-          f2unpack(x2, x0, x1);
-          if ((kPolyMask >> (pi & 7)) & 1) {
-            // exp2 on the FMA pipe: 2^x = 2^round(x) * poly(x - round(x)), |rel err| < 8e-5
-            const uint64_t xc = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
-            const uint64_t tt = fadd2(xc, kM);
-            const uint64_t fr = fsub2(xc, fsub2(tt, kM));
-            uint64_t pq = ffma2(fr, kC3, kC2);
-            pq = ffma2(pq, fr, kC1);
-            pq = ffma2(pq, fr, kC0);
-            float q0, q1, t0, t1;
-            f2unpack(pq, q0, q1);
-            f2unpack(tt, t0, t1);
-            p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
-            p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
-          } else {
-            p0 = ex2(x0);
-            p1 = ex2(x1);
+          for (int q = 0; q < 4; ++q) {
+            const int pi = kc * 4 + q;
+            const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * pi]), __uint_as_float(sr[2 * pi + 1])), c2, nm2);
+            float x0, x1, p0, p1;
+            f2unpack(x2, x0, x1);
+            if ((kPolyMask >> (pi & 7)) & 1) {
+              // exp2 on the FMA pipe: 2^x = 2^round(x) * poly(x - round(x)), |rel err| < 8e-5
+              const uint64_t xc = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+              const uint64_t tt = fadd2(xc, kM);
+              const uint64_t fr = fsub2(xc, fsub2(tt, kM));
+              uint64_t pq = ffma2(fr, kC3, kC2);
+              pq = ffma2(pq, fr, kC1);
+              pq = ffma2(pq, fr, kC0);
+              float q0, q1, t0, t1;
+              f2unpack(pq, q0, q1);
+              f2unpack(tt, t0, t1);
+              p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+              p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+            } else {
+              p0 = ex2(x0);
+              p1 = ex2(x1);
+            }
+            acc2[q] = fadd2(acc2[q], f2pack(p0, p1));
+            pp[(kc & 3) * 4 + q] = pack_bf16(p0, p1);
           }
-          acc2[q] = fadd2(acc2[q], f2pack(p0, p1));
-          pp[(kc & 3) * 4 + q] = pack_bf16(p0, p1);
+          if ((kc & 3) == 3) tmem_st16(s_tmem + kPCol + (kc >> 2) * 16, pp);
         }
-        if ((kc & 3) == 3) tmem_st16(s_tmem + kPCol + (kc >> 2) * 16, pp);
+        float a0, a1;
+        f2unpack(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])), a0, a1);
+        l_run += a0 + a1;
+        tmem_wait_st();  // P in TMEM before the MMA warp may read it
+        tc_fence_before();
+        mbar_arrive(p_full + t);
       }
-      float a0, a1;
-      f2unpack(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])), a0, a1);
-      l_run += a0 + a1;
-      tmem_wait_st();  // P in TMEM before the MMA warp may read it
-      tc_fence_before();
-      mbar_arrive(p_full + t);
-    }
-    // epilogue: O / l -> bf16 (or the split's f32 partial + log2-sum-exp2)
-    mbar_wait(o_ready + t, (nkv - 1) & 1);
-    tc_fence_after();
-    const int row = q0 + t * BQ + r;
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-    const bool live = row < p.seq_q;
-    if (!whole) {
-      const int64_t prow = (static_cast<int64_t>(tile - p.n_whole) * p.splits + split) * (2 * BQ) + t * BQ + r;
-      if (live) p.lse[prow] = m_run * c + __log2f(l_run);
-      float* orow = p.opart + prow * D;
+      // epilogue: O / l -> bf16 (or the split's f32 partial + log2-sum-exp2)
+      mbar_wait(o_ready + t, (kk * nkv + nkv - 1) & 1);
+      tc_fence_after();
+      const int row = q0 + t * BQ + r;
+      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+      const bool live = row < p.seq_q;
+      if (!whole) {
+        const int64_t prow = (static_cast<int64_t>(tile - p.n_whole) * p.splits + split) * (2 * BQ) + t * BQ + r;
+        if (live) p.lse[prow] = m_run * c + __log2f(l_run);
+        float* orow = p.opart + prow * D;
 #pragma unroll 1
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t u[32];
-        tmem_ld32(o_tmem + cc * 32, u);
-        tmem_wait_ld();
-        if (live) {
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t u[32];
+          tmem_ld32(o_tmem + cc * 32, u);
+          tmem_wait_ld();
+          if (live) {
 #pragma unroll
-          for (int g = 0; g < 8; ++g)
-            *reinterpret_cast<float4*>(orow + cc * 32 + 4 * g) =
-                make_float4(__uint_as_float(u[4 * g]) * inv, __uint_as_float(u[4 * g + 1]) * inv,
-                            __uint_as_float(u[4 * g + 2]) * inv, __uint_as_float(u[4 * g + 3]) * inv);
+            for (int g = 0; g < 8; ++g)
+              *reinterpret_cast<float4*>(orow + cc * 32 + 4 * g) =
+                  make_float4(__uint_as_float(u[4 * g]) * inv, __uint_as_float(u[4 * g + 1]) * inv,
+                              __uint_as_float(u[4 * g + 2]) * inv, __uint_as_float(u[4 * g + 3]) * inv);
+          }
         }
-      }
-    } else {
-      // O/l -> bf16 into this tile's Q buffer (idle once its last QK^T is done; same
-      // 128B-swizzled [64-col box][128 rows][128 B] layout), then TMA stores: coalesced,
-      // and under the Ulysses scatter straight into the owning ranks' buffers.
-      uint8_t* stile = sQ + t * C::kQBytes;
-      const uint32_t srow = smem_u32(stile) + r * 128;
-      const OutMap& m = p.out;
-      const int tr0 = q0 + t * BQ;  // first row of this tile
-      // TMA coordinates must be >= 0: a tile that starts in one rank's rows and ends in
-      // the next (or in the text rows) is written with direct stores instead.
-      const int64_t last = min(int64_t(tr0 + BQ - 1), int64_t(p.seq_q - 1));
-      const bool use_tma = tr0 < p.seq_q &&  // a tile wholly past the end stores nothing
-                           (m.nranks == 0 || tr0 >= m.text_row0 ||
-                            (last < m.text_row0 && tr0 / m.rows_per_rank == last / m.rows_per_rank));
+      } else {
+        // O/l -> bf16 into this tile's Q buffer (idle once its last QK^T is done; same
+        // 128B-swizzled [64-col box][128 rows][128 B] layout), then TMA stores: coalesced,
+        // and under the Ulysses scatter straight into the owning ranks' buffers.
+        uint8_t* stile = sQ + t * C::kQBytes;
+        const uint32_t srow = smem_u32(stile) + r * 128;
+        const OutMap& m = p.out;
+        const int tr0 = q0 + t * BQ;  // first row of this tile
+        // TMA coordinates must be >= 0: a tile that starts in one rank's rows and ends in
+        // the next (or in the text rows) is written with direct stores instead.
+        const int64_t last = min(int64_t(tr0 + BQ - 1), int64_t(p.seq_q - 1));
+        // Several blocks per CTA: direct stores, so the Q buffer is not needed for staging and
+        // the next block's Q loads while this one's softmax / PV / epilogue run.
+        const bool use_tma = npair == 1 && tr0 < p.seq_q &&  // a tile wholly past the end stores nothing
+                             (m.nranks == 0 || tr0 >= m.text_row0 ||
+                              (last < m.text_row0 && tr0 / m.rows_per_rank == last / m.rows_per_rank));
 #pragma unroll 1
-      for (int cc = 0; cc < D / 32; ++cc) {
-        uint32_t u[32];
-        tmem_ld32(o_tmem + cc * 32, u);
-        tmem_wait_ld();
-        uint4 pk[4];
-#pragma unroll
-        for (int g = 0; g < 4; ++g)
-          pk[g] = make_uint4(pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
-                             pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
-                             pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
-                             pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
-        if (use_tma) {
-          const uint32_t bx = srow + (cc >> 1) * (BQ * 128);
+        for (int cc = 0; cc < D / 32; ++cc) {
+          uint32_t u[32];
+          tmem_ld32(o_tmem + cc * 32, u);
+          tmem_wait_ld();
+          uint4 pk[4];
 #pragma unroll
           for (int g = 0; g < 4; ++g)
-            st_shared_v4(bx + ((((cc & 1) * 4 + g) ^ sw) << 4), pk[g].x, pk[g].y, pk[g].z, pk[g].w);
-        } else if (live && cc * 32 < p.head_dim) {
-          for_each_out(m, head, row, [&](__nv_bfloat16* orow) {
+            pk[g] = make_uint4(pack_bf16(__uint_as_float(u[8 * g]) * inv, __uint_as_float(u[8 * g + 1]) * inv),
+                               pack_bf16(__uint_as_float(u[8 * g + 2]) * inv, __uint_as_float(u[8 * g + 3]) * inv),
+                               pack_bf16(__uint_as_float(u[8 * g + 4]) * inv, __uint_as_float(u[8 * g + 5]) * inv),
+                               pack_bf16(__uint_as_float(u[8 * g + 6]) * inv, __uint_as_float(u[8 * g + 7]) * inv));
+          if (use_tma) {
+            const uint32_t bx = srow + (cc >> 1) * (BQ * 128);
 #pragma unroll
-            for (int g = 0; g < 4; ++g) *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = pk[g];
-          });
-        }
-      }
-      if (use_tma) {
-        fence_proxy_async_smem();
-        named_bar_sync(1 + t, 128);
-        if (quad == 0 && lane == 0) {
-          for (int c = 0; c < C::kBoxes; ++c) {
-            const uint8_t* src = stile + c * (BQ * 128);
-            if (m.nranks == 0)
-              tma_store_3d(&om.local, src, c * 64, head, tr0);
-            else if (tr0 >= m.text_row0)
-              for (int rr = 0; rr < m.nranks; ++rr) tma_store_3d(&om.txt[rr], src, c * 64, head, int(tr0 - m.text_row0));
-            else
-              tma_store_3d(&om.vid[tr0 / m.rows_per_rank], src, c * 64, head, int(tr0 % m.rows_per_rank));
+            for (int g = 0; g < 4; ++g)
+              st_shared_v4(bx + ((((cc & 1) * 4 + g) ^ sw) << 4), pk[g].x, pk[g].y, pk[g].z, pk[g].w);
+          } else if (live && cc * 32 < p.head_dim) {
+            for_each_out(m, head, row, [&](__nv_bfloat16* orow) {
+#pragma unroll
+              for (int g = 0; g < 4; ++g) *reinterpret_cast<uint4*>(orow + cc * 32 + 8 * g) = pk[g];
+            });
           }
-          bulk_commit();
-          bulk_wait<0>();  // complete (not just read out of smem) before the CTA exits
+        }
+        if (use_tma) {
+          fence_proxy_async_smem();
+          named_bar_sync(1 + t, 128);
+          if (quad == 0 && lane == 0) {
+            for (int c = 0; c < C::kBoxes; ++c) {
+              const uint8_t* src = stile + c * (BQ * 128);
+              if (m.nranks == 0)
+                tma_store_3d(&om.local, src, c * 64, head, tr0);
+              else if (tr0 >= m.text_row0)
+                for (int rr = 0; rr < m.nranks; ++rr)
+                  tma_store_3d(&om.txt[rr], src, c * 64, head, int(tr0 - m.text_row0));
+              else
+                tma_store_3d(&om.vid[tr0 / m.rows_per_rank], src, c * 64, head, int(tr0 % m.rows_per_rank));
+            }
+            bulk_commit();
+            bulk_wait<0>();  // complete (not just read out of smem) before the CTA exits
+          }
         }
       }
-    }
+    }  // block kk
   } else {
     setmaxnreg_dec<kCtrlRegs>();
   }
@@ -562,6 +608,25 @@ Plan choose_plan(int64_t seq_q, int64_t seq_kv, int heads, int head_dim) {
   return pl;
 }
 
+// Blocks per CTA for a short-KV launch with no split (see Params::pairs_per_cta): g
+// consecutive 256-query blocks of one head per CTA, K/V loaded once.  Cost in the
+// simulate() units: a block costs its KV blocks + 1 (Q load / epilogue bubble), a CTA
+// one more (prologue, K/V load); waves of CTAs over one slot per SM.  AQB_ATTN_PAIRS
+// forces g (1 = one block per CTA).
+static int choose_pairs_per_cta(int q_pairs, int heads, int nkv, int ring) {
+  if (2 * nkv > ring) return 1;  // K/V must stay resident in the ring
+  if (const char* e = getenv("AQB_ATTN_PAIRS")) return std::min(std::max(1, atoi(e)), q_pairs);
+  const int slots = sm_count();
+  int best = 1;
+  double bt = 1e30;
+  for (int g = 1; g <= 16 && g <= q_pairs; ++g) {
+    const int64_t ctas = int64_t(heads) * ((q_pairs + g - 1) / g);
+    const double t = double((ctas + slots - 1) / slots) * (g * (nkv + 1.0) + 1.0);
+    if (t < bt - 1e-9) bt = t, best = g;
+  }
+  return best;
+}
+
 static int64_t split_ws_bytes(int64_t tail_tiles, int splits, int head_dim) {
   if (splits <= 1 || tail_tiles <= 0) return 0;
   const int64_t rows = tail_tiles * splits * (2 * BQ);
@@ -639,7 +704,9 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
     memset(&om, 0, sizeof(om));
   }
   const int64_t tiles = static_cast<int64_t>(p.q_pairs) * p.heads;
-  const int64_t ctas = p.n_whole + (tiles - p.n_whole) * p.splits;
+  const int64_t ctas = p.pairs_per_cta > 1
+                           ? int64_t(p.heads) * ((p.q_pairs + p.pairs_per_cta - 1) / p.pairs_per_cta)
+                           : p.n_whole + (tiles - p.n_whole) * p.splits;
   AQB_CUDA_TRY(launch_pdl(kern, dim3(unsigned(ctas)), dim3(kThreads), smem, stream, tq, tk, tv, om, p));
   AQB_LAUNCH_CHECK();
   if (p.n_whole < tiles) {
@@ -693,6 +760,8 @@ static int run(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t l
   p.splits = plan.splits;
   p.kv_blocks_per_split = plan.per;
   p.part_d = head_dim <= 64 ? 64 : 128;
+  const int ring = head_dim == 128 ? Cfg<128>::NS : Cfg<64>::NS;
+  p.pairs_per_cta = plan.n_whole == tiles ? choose_pairs_per_cta(p.q_pairs, heads, nkv, ring) : 1;
   if (plan.n_whole < tiles) {
     float* ws = reinterpret_cast<float*>(workspace);
     p.lse = ws;
@@ -720,6 +789,15 @@ extern "C" int64_t aqb_attention_auto_workspace_bytes(int64_t seq_q, int64_t seq
 
 extern "C" int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim) {
   return aqb::attn::choose_plan(seq_q, seq_kv, heads, head_dim).splits;
+}
+
+extern "C" int aqb_attention_pairs_per_cta(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim) {
+  using namespace aqb::attn;
+  const Plan pl = choose_plan(seq_q, seq_kv, heads, head_dim);
+  const int q_pairs = int((seq_q + 2 * BQ - 1) / (2 * BQ));
+  if (pl.n_whole != int64_t(q_pairs) * heads) return 1;
+  const int nkv = int((seq_kv + BKV - 1) / BKV);
+  return choose_pairs_per_cta(q_pairs, heads, nkv, head_dim == 128 ? Cfg<128>::NS : Cfg<64>::NS);
 }
 
 extern "C" int aqb_attention_whole_tiles(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim) {

@@ -191,6 +191,18 @@ def main():
             res.append(attn_case(S, S, heads, 128))
         res.append(attn_case(25440 + 256, 25440 + 256, 6, 128))
         res.append(attn_case(118800 + 256, 118800 + 256, 3, 128))
+    if args.only == "attn-cross":  # cross-attention to 256 text tokens: query blocks per CTA (K/V resident)
+        import os
+        for rows, heads in ((S, 16), (S // 2, 8), (S // 4, 4), (S // 8, 2)):
+            for g in ("1", "2", "3", "4", "6", "8", None):
+                if g is None:
+                    os.environ.pop("AQB_ATTN_PAIRS", None)
+                else:
+                    os.environ["AQB_ATTN_PAIRS"] = g
+                r = attn_case(rows, 256, heads, 128)
+                r["pairs_per_cta"] = g or "auto"
+                res.append(r)
+        os.environ.pop("AQB_ATTN_PAIRS", None)
     if args.only == "attn-long":  # config 4 per rank at P=8 (and the 1-GPU per-head shape)
         res.append(attn_case(118800 + 256, 118800 + 256, 3, 128, args.ncu))
     if args.only in ("all", "norm"):

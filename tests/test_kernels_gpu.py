@@ -358,6 +358,60 @@ def test_attention_split_kv(sq, skv, heads, d, splits):
     assert rel_l2(o2, o1) < 8e-3
 
 
+@pytest.mark.parametrize("sq,skv,heads,d,g", [(7800, 256, 16, 128, None), (3000, 77, 3, 128, 3),
+                                               (1000, 300, 2, 64, 2), (2100, 256, 2, 128, 5), (129, 16, 4, 128, 2),
+                                               (4000, 256, 1, 128, 16)])
+def test_attention_multi_block_ctas(sq, skv, heads, d, g, monkeypatch):
+    """Short KV: CTAs that run several 256-query blocks with K/V resident give bit-identical
+    outputs to one block per CTA (same per-tile math), and match the oracle."""
+    gen = torch.Generator(device=dev).manual_seed(sq + 3 * skv)
+    q = torch.randn(sq, heads * d, device=dev, generator=gen).to(torch.bfloat16)
+    k = torch.randn(skv, heads * d, device=dev, generator=gen).to(torch.bfloat16)
+    v = torch.randn(skv, heads * d, device=dev, generator=gen).to(torch.bfloat16)
+    monkeypatch.setenv("AQB_ATTN_PAIRS", "1")
+    o1 = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
+    ops.attention(q, k, v, o1, heads, d)
+    if g is None:
+        monkeypatch.delenv("AQB_ATTN_PAIRS")
+        from paper_2505_10584_b200 import _native
+        assert _native.query("aqb_attention_pairs_per_cta", sq, skv, heads, d) > 1
+    else:
+        monkeypatch.setenv("AQB_ATTN_PAIRS", str(g))
+    o2 = torch.full_like(o1, 7.0)
+    ops.attention(q, k, v, o2, heads, d)
+    torch.cuda.synchronize()
+    assert torch.equal(o1, o2)
+    exp = _attn_ref(q.view(sq, heads, d), k.view(skv, heads, d), v.view(skv, heads, d))
+    assert rel_l2(o2, exp) < 1e-2
+
+
+@pytest.mark.parametrize("g,P,rpr,St,hl", [(3, 4, 300, 40, 2), (2, 2, 1000, 256, 4), (4, 4, 1950, 256, 4)])
+def test_attention_scatter_multi_block(g, P, rpr, St, hl, monkeypatch):
+    """Cross-attention (256 text K/V rows) through the scatter epilogue with several query
+    blocks per CTA: every rank's rows equal the local one-block-per-CTA result."""
+    d, skv = 128, 256
+    H = P * hl * d
+    sq = P * rpr + St
+    gen = torch.Generator(device=dev).manual_seed(17 + g)
+    q = torch.randn(sq, hl * d, device=dev, generator=gen).to(torch.bfloat16)
+    kv = torch.randn(skv, 2, hl * d, device=dev, generator=gen).to(torch.bfloat16).view(skv, -1)
+    monkeypatch.setenv("AQB_ATTN_PAIRS", "1")
+    ref_o = torch.empty(sq, hl * d, device=dev, dtype=torch.bfloat16)
+    ops.attention(q, kv, kv[:, hl * d:], ref_o, hl, d)
+    monkeypatch.setenv("AQB_ATTN_PAIRS", str(g))
+    outs = [torch.zeros(rpr + St, H, device=dev, dtype=torch.bfloat16) for _ in range(P)]
+    rank = P - 1
+    ops.attention_scatter(q, kv, kv[:, hl * d:], [o.data_ptr() + rank * hl * d * 2 for o in outs], H, hl, d, rpr,
+                          P * rpr)
+    torch.cuda.synchronize()
+    cols = slice(rank * hl * d, (rank + 1) * hl * d)
+    for r in range(P):
+        assert torch.equal(outs[r][:rpr, cols], ref_o[r * rpr:(r + 1) * rpr])
+        if St:
+            assert torch.equal(outs[r][rpr:, cols], ref_o[P * rpr:])
+        assert float(outs[r][:, :rank * hl * d].abs().sum()) == 0.0
+
+
 def _native_splits(sq, skv, heads, d):
     from paper_2505_10584_b200 import _native
     return _native.query("aqb_attention_splits", sq, skv, heads, d)

@@ -78,6 +78,11 @@ def test_attention_split_planner_and_workspace_without_gpu(lib_path):
                                                                           tail_rows * 128) * 4
     assert lib.aqb_attention_whole_tiles(7800, 7800, 8, 128) == 248  # 248 tiles: splitting never pays
     assert lib.aqb_attention_auto_workspace_bytes(7800, 7800, 8, 128) == 0
+    # cross-attention to 256 text tokens (K/V resident): 4 blocks of 256 queries per CTA,
+    # 16 heads x 8 CTAs = 128 CTAs in one wave (was 496 one-block CTAs in 4 waves)
+    assert lib.aqb_attention_pairs_per_cta(7800, 256, 16, 128) == 4
+    assert lib.aqb_attention_pairs_per_cta(7800, 7800, 16, 128) == 1  # K/V streamed: one block per CTA
+    assert lib.aqb_attention_pairs_per_cta(300, 256, 2, 128) == 1     # 4 CTAs: nothing to amortise
 
 
 def test_peer_barrier_validates_before_launch(lib_path):
