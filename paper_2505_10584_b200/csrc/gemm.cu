@@ -921,12 +921,15 @@ static int pick_variant(int64_t m, int64_t n, int64_t k, bool f32_out = false) {
     if (t < best * 0.97) best = t, bv = c.v;
   }
   // f32-output epilogues (gate*residual, reduce-scatter) on a shard small enough that the
-  // 256x256 pair tiles fill at most one wave: nothing overlaps the exposed f32 epilogue,
-  // and 256x128 pair tiles (twice the CTAs, half the epilogue each) measured faster:
-  // 1950x2048x2048 515 -> 592 TFLOP/s, 975x2048x8192 561 -> 821.
+  // 256x256 pair tiles fill at most one wave (or two with a short K): little overlaps the
+  // exposed f32 epilogue, and 256x128 pair tiles (twice the CTAs, half the epilogue each)
+  // measured faster: 1950x2048x2048 515 -> 592 TFLOP/s, 975x2048x8192 561 -> 821; two
+  // waves, K = 2048: 3900x2048x2048 44.0 -> 39.9 us, with the bf16 residual copy 50.0 ->
+  // 48.0; but K = 8192 keeps the pair tiles (3900x2048x8192 99.2 vs 113.5 us;
+  // `scripts/kernel_bench.py --only gemm-variants`).
   if (f32_out && bv == V2_256) {
     const double tiles = double((m + 255) / 256) * double((n + 255) / 256);
-    if (tiles <= sms / 2) bv = V2_128;
+    if (tiles <= sms / 2 || (tiles <= sms && k <= 4096)) bv = V2_128;
   }
   return bv;
 }

@@ -1,0 +1,4 @@
+for v in default 2cta256 2cta128; do
+  if [ $v = default ]; then unset AQB_GEMM_VARIANT; else export AQB_GEMM_VARIANT=$v; fi
+  timeout 120 python scripts/kernel_bench.py --only gemm-variants | sed "s/^{/{\"variant\": \"$v\", /" >> gpurun_out/kb_gemm_variants2.log 2>&1
+done

@@ -191,6 +191,12 @@ def main():
             res.append(attn_case(S, S, heads, 128))
         res.append(attn_case(25440 + 256, 25440 + 256, 6, 128))
         res.append(attn_case(118800 + 256, 118800 + 256, 3, 128))
+    if args.only == "gemm-variants":  # H-wide projections (K = H) of config 2 at 1 / 2 / 4 GPUs (AQB_GEMM_VARIANT sweeps)
+        for m in (S, S // 2, S // 4):
+            res.append(gemm_case(m, H, H, "gate_res"))
+            res.append(gemm_case(m, H, H, "bf16"))
+            res.append(proj_aux_case(m, H, H))
+            res.append(gemm_case(m, H, 4 * H, "gate_res"))
     if args.only == "attn-cross":  # cross-attention to 256 text tokens: query blocks per CTA (K/V resident)
         import os
         for rows, heads in ((S, 16), (S // 2, 8), (S // 4, 4), (S // 8, 2)):
