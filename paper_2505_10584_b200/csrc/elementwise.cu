@@ -52,6 +52,31 @@ struct Outs {
   int n;
 };
 
+// y = LN(x) * (1 + scale) + shift as t = x*rstd - mean*rstd, y = t*scale + (t + shift):
+// 3 FP ops per element (the SASS of the plain form spent a third of its issue slots on
+// the per-row 1 + scale)
+AQB_DEV float4 modulate4(float4 x, float rstd, float nmr, float4 sc, float4 sh) {
+  float4 o;
+  float t;
+  t = fmaf(x.x, rstd, nmr), o.x = fmaf(t, sc.x, t + sh.x);
+  t = fmaf(x.y, rstd, nmr), o.y = fmaf(t, sc.y, t + sh.y);
+  t = fmaf(x.z, rstd, nmr), o.z = fmaf(t, sc.z, t + sh.z);
+  t = fmaf(x.w, rstd, nmr), o.w = fmaf(t, sc.w, t + sh.w);
+  return o;
+}
+
+// one destination: the pointer stays in the parameter space (a dynamic index into
+// Outs::p put it in local memory: an LDL per store)
+template <typename OutT>
+AQB_DEV void store_outs(const Outs<OutT>& ys, int64_t off, float4 o) {
+  if (ys.n == 1) {
+    store4(ys.p[0] + off, o);
+    return;
+  }
+#pragma unroll 1
+  for (int d = 0; d < ys.n; ++d) store4(ys.p[d] + off, o);
+}
+
 // OutT = bf16 (product path) or float (fp32 validation mode).
 template <int NV, typename OutT>
 __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__ x, int64_t ldx,
@@ -90,6 +115,7 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
   }
   const float4* sh4 = reinterpret_cast<const float4*>(shift);
   const float4* sc4 = reinterpret_cast<const float4*>(scale);
+  const float nmr = -mean * rstd;
   const int64_t yoff = row * ldy;
   float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
   float dsum = 0.f, psum = 0.f;
@@ -98,13 +124,8 @@ __global__ void __launch_bounds__(256) norm_mod_kernel(const float* __restrict__
     const int c4 = lane + 32 * j;
     const float4 sc = scale ? __ldg(sc4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 sh = shift ? __ldg(sh4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 o;
-    o.x = (v[j].x - mean) * rstd * (1.f + sc.x) + sh.x;
-    o.y = (v[j].y - mean) * rstd * (1.f + sc.y) + sh.y;
-    o.z = (v[j].z - mean) * rstd * (1.f + sc.z) + sh.z;
-    o.w = (v[j].w - mean) * rstd * (1.f + sc.w) + sh.w;
-#pragma unroll 1
-    for (int d = 0; d < ys.n; ++d) store4(ys.p[d] + yoff + 4 * c4, o);
+    const float4 o = modulate4(v[j], rstd, nmr, sc, sh);
+    store_outs(ys, yoff + 4 * c4, o);
     if (pr) {
       const float4 p = pr[c4];
       dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
@@ -215,6 +236,7 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
   }
   const float4* sh4 = reinterpret_cast<const float4*>(shift);
   const float4* sc4 = reinterpret_cast<const float4*>(scale);
+  const float nmr = -mean * rstd;
   const int64_t yoff = row * ldy;
   float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
   float dsum = 0.f, psum = 0.f;
@@ -223,13 +245,8 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
     const int c4 = tid + T * j;
     const float4 sc = scale ? __ldg(sc4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
     const float4 sh = shift ? __ldg(sh4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    float4 o;
-    o.x = (v[j].x - mean) * rstd * (1.f + sc.x) + sh.x;
-    o.y = (v[j].y - mean) * rstd * (1.f + sc.y) + sh.y;
-    o.z = (v[j].z - mean) * rstd * (1.f + sc.z) + sh.z;
-    o.w = (v[j].w - mean) * rstd * (1.f + sc.w) + sh.w;
-#pragma unroll 1
-    for (int d = 0; d < ys.n; ++d) store4(ys.p[d] + yoff + 4 * c4, o);
+    const float4 o = modulate4(v[j], rstd, nmr, sc, sh);
+    store_outs(ys, yoff + 4 * c4, o);
     if (pr) {
       const float4 p = pr[c4];
       dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
