@@ -28,6 +28,33 @@ import torch.nn.functional as F
 f32 = torch.float32
 
 
+class strict_fp32:
+    """Context manager: fp32 matmuls in full fp32 on a GPU (no TF32), restored on exit."""
+
+    def __enter__(self):
+        self.saved = (torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32,
+                      torch.get_float32_matmul_precision())
+        torch.backends.cuda.matmul.allow_tf32 = False
+        torch.backends.cudnn.allow_tf32 = False
+        torch.set_float32_matmul_precision("highest")
+        return self
+
+    def __exit__(self, *exc):
+        torch.backends.cuda.matmul.allow_tf32, torch.backends.cudnn.allow_tf32, prec = self.saved
+        torch.set_float32_matmul_precision(prec)
+        return False
+
+
+def _strict(fn):
+    import functools
+
+    @functools.wraps(fn)
+    def run(*a, **kw):
+        with strict_fp32():
+            return fn(*a, **kw)
+    return run
+
+
 def _w(W, name):
     return W[name].to(f32)
 
@@ -90,13 +117,31 @@ def gelu(x):
     return F.gelu(x, approximate="tanh")
 
 
+SCORE_CHUNK = 1 << 27  # score elements materialised at once (512 MB fp32)
+
+
 def attention(q, k, v):
-    """softmax(q kᵀ/√D) v per head; q [Sq,A,D], k/v [Skv,A,D] -> [Sq, A·D]."""
-    D = q.shape[-1]
-    s = torch.einsum("qad,kad->aqk", q, k) / math.sqrt(D)
-    p = torch.softmax(s, dim=-1)
-    o = torch.einsum("aqk,kad->qad", p, v)
-    return o.reshape(q.shape[0], -1)
+    """softmax(q kᵀ/√D) v per head; q [Sq,A,D], k/v [Skv,A,D] -> [Sq, A·D].
+
+    Exact softmax over every key of a query row; long sequences (the 119k-token
+    configs) are processed one head and one block of query rows at a time so the
+    score matrix never exceeds ``SCORE_CHUNK`` elements — the same arithmetic,
+    bounded memory."""
+    Sq, A, D = q.shape
+    Skv = k.shape[0]
+    if A * Sq * Skv <= SCORE_CHUNK:
+        s = torch.einsum("qad,kad->aqk", q, k) / math.sqrt(D)
+        p = torch.softmax(s, dim=-1)
+        o = torch.einsum("aqk,kad->qad", p, v)
+        return o.reshape(Sq, -1)
+    out = torch.empty(Sq, A, D, dtype=q.dtype, device=q.device)
+    rows = max(1, SCORE_CHUNK // Skv)
+    for a in range(A):
+        kt, va = k[:, a].t(), v[:, a]
+        for r0 in range(0, Sq, rows):
+            s = (q[r0:r0 + rows, a] @ kt) / math.sqrt(D)
+            out[r0:r0 + rows, a] = torch.softmax(s, dim=-1) @ va
+    return out.reshape(Sq, -1)
 
 
 def silu(x):
@@ -233,20 +278,52 @@ class OracleDiT:
     """
 
     def __init__(self, cfg, weights: dict, text: torch.Tensor, pooled: torch.Tensor | None, grid, n_front=None,
-                 mode: str = "dit-layer-cache"):
+                 mode: str = "dit-layer-cache", device="cpu"):
+        """``device``: where the fp32 restatement runs — ``"cpu"`` (the reference CPU path)
+        or a CUDA device for the full-depth / full-geometry parity tests, in strict fp32
+        (TF32 off for every matmul while this oracle computes, see :func:`strict_fp32`)."""
         self.cfg = cfg
         self.mode = mode
-        self.W = {k: v.detach().to("cpu", f32) for k, v in weights.items()}
-        self.text = text.to("cpu", f32)
-        self.pooled = None if pooled is None else pooled.to("cpu", f32)
+        self.device = torch.device(device)
+        self.W = {k: v.detach().to(self.device, f32) for k, v in weights.items()}
+        self.text = text.to(self.device, f32)
+        self.pooled = None if pooled is None else pooled.to(self.device, f32)
         self.grid = tuple(grid)
-        self.ang = rope_angles(self.grid, cfg.rope_dims, cfg.rope_theta)
+        self.ang = rope_angles(self.grid, cfg.rope_dims, cfg.rope_theta).to(self.device)
         self.n_front = cfg.num_layers if n_front is None else n_front
 
     def _temb(self, t):
         W = self.W
-        h = silu(linear(W, "t_emb.fc1", timestep_features(t, self.cfg.freq_dim)))
+        h = silu(linear(W, "t_emb.fc1", timestep_features(t, self.cfg.freq_dim).to(self.device)))
         return linear(W, "t_emb.fc2", h)
+
+    def run_blocks(self, x_tok, t, ids):
+        """Embed, blocks ``ids`` (in that order, any indices), final layer — the CPU
+        baseline's per-block timing sample; every block runs at full size on its own
+        weights.  Returns the velocity-shaped output."""
+        cfg, W = self.cfg, self.W
+        n = x_tok.shape[0]
+        t0 = self._temb(t)
+        if cfg.family == "single-dit":
+            tmod = linear(W, "t_block", silu(t0))
+            x = linear(W, "x_emb", x_tok)
+            for i in ids:
+                x, _ = single_dit_block(W, i, x, tmod, self.text, cfg, self.ang)
+            fin = _w(W, "final.table").reshape(2, -1) + t0
+            return linear(W, "final", modulate(x, fin[0], fin[1], cfg.norm_eps))
+        vec = t0 + linear(W, "p_emb.fc2", silu(linear(W, "p_emb.fc1", self.pooled)))
+        img, txt, x = linear(W, "x_emb", x_tok), linear(W, "txt_in", self.text), None
+        for i in ids:
+            if i < cfg.num_dual:
+                src = (img, txt) if x is None else (x[:n], x[n:])
+                img, txt = mm_dual_block(W, i, *src, vec, cfg, self.ang)[:2]
+                x = None
+            else:
+                x = torch.cat([img, txt]) if x is None else x
+                x, _ = mm_single_block(W, i - cfg.num_dual, x, vec, cfg, self.ang)
+                img, txt = x[:n], x[n:]
+        fm = linear(W, "final.mod", silu(vec)).reshape(2, -1)
+        return linear(W, "final", modulate(img, fm[0], fm[1], cfg.norm_eps))
 
     def velocity(self, x_tok, t, full=True, state=None, blocks=None):
         cfg, W = self.cfg, self.W
@@ -312,6 +389,7 @@ def rel_l1(m, m_prev) -> float:
     return float((m.double() - m_prev.double()).abs().sum() / m_prev.double().abs().sum())
 
 
+@_strict
 def denoise(model: OracleDiT, x0_lat: torch.Tensor, num_steps: int, flags=None, policy=None,
             return_all=True):
     """Euler flow-matching sampler t_i = i/N, x += (1/N)·v (fitted).
@@ -321,9 +399,9 @@ def denoise(model: OracleDiT, x0_lat: torch.Tensor, num_steps: int, flags=None, 
     ``(latents per step [N+1], flags taken, rel values)``.
     """
     cfg = model.cfg
-    x = patchify(x0_lat.to(f32), cfg.patch)
+    x = patchify(x0_lat.to(model.device, f32), cfg.patch)
     state = {}
-    lat = [x0_lat.to(f32)]
+    lat = [x0_lat.to("cpu", f32)]
     taken, rels = [], []
     acc = 0.0
     m_prev = None
@@ -343,9 +421,9 @@ def denoise(model: OracleDiT, x0_lat: torch.Tensor, num_steps: int, flags=None, 
         taken.append(full)
         x = x + (1.0 / num_steps) * v
         if return_all:
-            lat.append(unpatchify(x, model.grid, cfg.patch, cfg.latent_channels))
+            lat.append(unpatchify(x, model.grid, cfg.patch, cfg.latent_channels).cpu())
     if not return_all:
-        lat.append(unpatchify(x, model.grid, cfg.patch, cfg.latent_channels))
+        lat.append(unpatchify(x, model.grid, cfg.patch, cfg.latent_channels).cpu())
     return lat, taken, rels
 
 
@@ -369,6 +447,7 @@ def _probe(model: OracleDiT, x_tok, t):
     return modulate(img, mi[0], mi[1], cfg.norm_eps), None
 
 
+@_strict
 def denoise_windows(models, x0_lat: torch.Tensor, num_steps: int, clips, flags=None):
     """Temporal MultiDiffusion (Eq. 3) — fp32 restatement.
 
@@ -379,10 +458,10 @@ def denoise_windows(models, x0_lat: torch.Tensor, num_steps: int, clips, flags=N
     after every step (``num_steps + 1`` entries).
     """
     cfg = models[0].cfg
-    x = x0_lat.to(f32).clone()
+    x = x0_lat.to(models[0].device, f32).clone()
     states = [{} for _ in clips]
-    out = [x.clone()]
-    count = torch.zeros(x.shape[1])
+    out = [x.cpu()]
+    count = torch.zeros(x.shape[1], device=x.device)
     for s, e in clips:
         count[s:e] += 1
     for i in range(num_steps):
@@ -395,5 +474,5 @@ def denoise_windows(models, x0_lat: torch.Tensor, num_steps: int, clips, flags=N
             tok = tok + (1.0 / num_steps) * v
             acc[:, s:e] += unpatchify(tok, m.grid, cfg.patch, cfg.latent_channels)
         x = acc / count[None, :, None, None]
-        out.append(x.clone())
+        out.append(x.cpu())
     return out

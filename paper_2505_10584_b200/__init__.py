@@ -8,14 +8,16 @@ Public API (drop-in for the reference's cache-schedule boundary,
   ``composite_speedup``, ``ConfigError``, ``PlanningError``, ``DimensionError``
 * ``plan_vae_tiles`` / ``TilePlan`` / ``Tile`` and ``plan_temporal_windows`` /
   ``WindowPlan`` (``inference.py:89-279``), with GPU blend / Eq. 3 kernels
+* geometry ``Bucket`` / ``LatentShape`` / ``VaeSpec`` / ``latent_shape`` /
+  ``token_count`` / ``snap_bucket`` (``buckets.py:17-122``)
 * the planner formulas the path is sized by: ``ModelArch``, ``TABLE2_FIT``,
   ``estimate_param_count``, ``flops_per_microstep``, ``tp_sp_layer_comm``,
   ``cp_gate_and_comm`` / ``CP_TOKEN_GATE``, ``ChunkSpec`` / ``ChunkTable`` /
-  ``BUILTIN_CHUNKS`` (``config.py``, ``presets.py``, ``simulate.py``, ``comm.py``,
+  ``BUILTIN_CHUNKS`` / ``load_chunk_table``, ``resolved_param_count`` (``config.py``, ``presets.py``, ``simulate.py``, ``comm.py``,
   ``memory.py``; see ``planner.py``)
 * new: ``RelL1Policy``, ``DiTConfig`` + presets, ``SingleDiT`` / ``MMDiT``
   (model construction), ``denoise`` (sampler loop), ``denoise_windows``
-  (temporal MultiDiffusion), ``latent_shape``, ``token_count``; multi-GPU
+  (temporal MultiDiffusion); multi-GPU
   groups ``Ulysses`` (sequence parallel) and ``TensorSP`` (TP-SP, Single-DiT).
 
 The model/sampler symbols need CUDA and ``libaqb.so`` (hand-written sm_100a
@@ -27,13 +29,18 @@ from .config import (
     PRESETS,
     SINGLE_DIT_2B,
     TINY_MM,
+    Bucket,
+    LatentShape,
     TINY_SINGLE,
     DiTConfig,
     VaeSpec,
     VideoSpec,
     flops_per_step,
     latent_shape,
+    snap_bucket,
+    snap_to_multiple,
     token_count,
+    video_token_count,
 )
 from .errors import ConfigError, DimensionError, NativeError, PlanningError
 from .schedule import (
@@ -60,6 +67,8 @@ from .planner import (
     cp_gate_and_comm,
     estimate_param_count,
     flops_per_microstep,
+    load_chunk_table,
+    resolved_param_count,
     tp_sp_layer_comm,
 )
 
@@ -92,6 +101,8 @@ __all__ = [
     "DiTConfig", "MM_DIT_13B", "NativeError", "PRESETS", "PlanningError", "RelL1Policy", "SINGLE_DIT_2B",
     "TINY_MM", "TINY_SINGLE", "VaeSpec", "VideoSpec", "composite_speedup", "dit_parallel_latency",
     "flops_per_step", "front_block_count", "latent_shape", "no_cache", "plan_cache", "token_count",
+    "Bucket", "LatentShape", "snap_bucket", "snap_to_multiple", "video_token_count",
+    "load_chunk_table", "resolved_param_count",
     "SingleDiT", "MMDiT", "SingleDiTTP", "build_model", "denoise", "DenoiseResult", "denoise_windows",
     "Ulysses", "TensorSP",
     "Tile", "TilePlan", "WindowPlan", "plan_vae_tiles", "plan_temporal_windows",

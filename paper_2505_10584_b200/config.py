@@ -6,7 +6,8 @@
   the reference never had: the family (Single-DiT / MM-DiT, ``PAPER.md:15-17,
   103,106``), the dual/single split, text dims, 3D-RoPE split and base.
   Everything not published is a builder choice ("fitted").
-* :func:`latent_shape` / :func:`token_count` restate ``buckets.py:65-98``.
+* :class:`Bucket`, :class:`LatentShape`, :func:`latent_shape`, :func:`token_count`,
+  :func:`snap_bucket` restate ``buckets.py:33-122`` (same signatures and result types).
 * :func:`flops_per_step` follows the reference convention
   ``simulate.py:60-73`` (4·S²·H attention + 2·S·(4+2·ffn)·H² linears per
   layer + head), extended with the Single-DiT cross-attention term.
@@ -53,10 +54,78 @@ def latent_shape(frames: int, height: int, width: int, vae: VaeSpec = VaeSpec())
     return (1 + (frames - 1) // vae.temporal_ratio, height // vae.spatial_ratio, width // vae.spatial_ratio)
 
 
-def token_count(frames: int, height: int, width: int, patch=(1, 2, 2), vae: VaeSpec = VaeSpec()) -> int:
-    """Post-patchify tokens, ceiling division per axis — ``buckets.py:89-98``."""
+@dataclass(frozen=True)
+class Bucket:
+    """One shape class of videos: ``{batch, frames, height, width}`` (``buckets.py:33-51``)."""
+
+    batch: int
+    frames: int
+    height: int
+    width: int
+
+    def __post_init__(self):
+        for name in ("batch", "frames", "height", "width"):
+            if getattr(self, name) < 1:
+                raise ConfigError("must be >= 1", f"bucket.{name}")
+
+    def key(self) -> tuple[int, int, int, int]:
+        return (self.batch, self.frames, self.height, self.width)
+
+    def label(self) -> str:
+        return f"{{{self.batch},{self.frames},{self.height},{self.width}}}"
+
+
+@dataclass(frozen=True)
+class LatentShape:
+    """Latent geometry of one video plus its post-patchify token counts (``buckets.py:54-62``)."""
+
+    t_lat: int
+    h_lat: int
+    w_lat: int
+    tokens: int
+    tokens_batch: int
+
+
+def _patch_of(arch) -> tuple[int, int, int]:
+    """Patch dims of a planner ``ModelArch`` (``patch_t/h/w``) or an executable ``DiTConfig``
+    (``patch``); the reference default 1x2x2 when ``arch`` is None (``buckets.py:91``)."""
+    if arch is None:
+        return (1, 2, 2)
+    if hasattr(arch, "patch_t"):
+        return (arch.patch_t, arch.patch_h, arch.patch_w)
+    return tuple(arch.patch)
+
+
+def token_count(bucket: Bucket, vae: VaeSpec = VaeSpec(), arch=None) -> LatentShape:
+    """Tokens per video (post-patchify, ceiling division per axis) and per batch —
+    ``buckets.py:89-98``, same signature and result type."""
+    pt, ph, pw = _patch_of(arch)
+    t_lat, h_lat, w_lat = latent_shape(bucket.frames, bucket.height, bucket.width, vae)
+    tokens = math.ceil(t_lat / pt) * math.ceil(h_lat / ph) * math.ceil(w_lat / pw)
+    return LatentShape(t_lat=t_lat, h_lat=h_lat, w_lat=w_lat, tokens=tokens, tokens_batch=bucket.batch * tokens)
+
+
+def video_token_count(frames: int, height: int, width: int, patch=(1, 2, 2), vae: VaeSpec = VaeSpec()) -> int:
+    """Tokens of one ``frames x height x width`` video (the int :func:`token_count` gives as
+    ``.tokens`` for a batch-1 bucket)."""
+    pt, ph, pw = patch
     t, h, w = latent_shape(frames, height, width, vae)
-    return math.ceil(t / patch[0]) * math.ceil(h / patch[1]) * math.ceil(w / patch[2])
+    return math.ceil(t / pt) * math.ceil(h / ph) * math.ceil(w / pw)
+
+
+def snap_to_multiple(value: int, multiple: int) -> int:
+    """Nearest positive multiple, ties round up (``buckets.py:101-104``)."""
+    return max(multiple, int(multiple * math.floor(value / multiple + 0.5)))
+
+
+def snap_bucket(bucket: Bucket, vae: VaeSpec = VaeSpec(), arch=None) -> Bucket:
+    """Round height/width to the VAE x patch grain (480x854 -> 480x848), ``buckets.py:107-122``."""
+    _, ph, pw = _patch_of(arch)
+    height = snap_to_multiple(bucket.height, vae.spatial_ratio * ph)
+    width = snap_to_multiple(bucket.width, vae.spatial_ratio * pw)
+    if (height, width) == (bucket.height, bucket.width):
+        return bucket
+    return Bucket(bucket.batch, bucket.frames, height, width)
 
 
 @dataclass(frozen=True)

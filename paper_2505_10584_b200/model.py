@@ -235,6 +235,15 @@ class DiTModel:
         """False if a peer barrier timed out (a rank never arrived) since prepare()."""
         return self.peer is None or int(self.peer_status.item()) == 0
 
+    def close(self):
+        """Release the symmetric peer buffers (collective under a multi-rank group; drop any
+        CUDA graph that captured this model first — it holds their addresses)."""
+        for name in ("peer_ocache", "peer"):
+            pb = self.__dict__.pop(name, None)
+            if pb is not None:
+                pb.close()
+        self.peer = None
+
     # ------------------------------------------------------------- primitives
     def _mod(self, name):
         H = self.cfg.hidden_size
@@ -470,11 +479,14 @@ class DiTModel:
 
     # ------------------------------------------------------------------ steps
     def reset(self, x0: torch.Tensor, num_steps: int, policy=None, cache_mode: str = "dit-layer-cache",
-              frame_offset: int | None = None):
+              frame_offset: int | None = None, cached_cost_fraction: float | None = None):
         """Load the initial latent [C, T, H, W] and the Euler grid t_i = i/N.
 
         ``cache_mode``: ``dit-layer-cache`` (rear-block offset reuse) or
         ``attention-cache`` (per-block attention-output reuse).
+        ``cached_cost_fraction``: the schedule's cost of a cached step (``inference.py:77``);
+        under ``dit-layer-cache`` a cached step runs the front ``ceil(fraction·L)`` blocks, so
+        the split follows the schedule the caller passes (default: the constructor's).
         ``frame_offset``: ``x0`` is a longer latent and this model's clip starts at that
         latent frame (temporal MultiDiffusion)."""
         cfg, g = self.cfg, self.geo
@@ -485,6 +497,8 @@ class DiTModel:
         if cache_mode == "attention-cache" and self._tp():
             raise ConfigError("attention-cache mode is not implemented under TP-SP", "cache.mode")
         self.cache_mode = cache_mode
+        if cached_cost_fraction is not None:
+            self.n_front = front_block_count(cfg.num_layers, cached_cost_fraction)
         if cache_mode == "attention-cache":
             self._alloc_attention_cache()
         C = cfg.latent_channels

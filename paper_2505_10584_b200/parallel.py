@@ -285,10 +285,17 @@ class PeerBuffers:
         return [p + int(offset_bytes) for p in self._all[name]]
 
     def close(self):
-        """Unmap peers and free this rank's buffers (collective: barrier first)."""
-        dist.barrier(group=self.sp.group)
+        """Unmap peers and free this rank's buffers (collective).
+
+        Drain this rank's queued kernels first (its scatter epilogues and barrier signals
+        store into the peers' buffers), then the host barrier: once every rank has passed
+        it, no kernel anywhere can still write into the memory freed below (with gloo the
+        barrier is host-only, so the device drain must come before it)."""
+        if not self._own and not self._opened:
+            return
         if self.device.type == "cuda":
             torch.cuda.synchronize(self.device)
+        dist.barrier(group=self.sp.group)
         for p in self._opened:
             _native.call("aqb_peer_close", p)
         for p in self._own.values():

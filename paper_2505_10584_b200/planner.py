@@ -20,7 +20,9 @@ them here too.  Each is checked against values produced by the reference itself
 
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
+from pathlib import Path
 
 from .errors import ConfigError
 
@@ -98,6 +100,13 @@ def estimate_param_count(arch: ModelArch, latent_channels: int = 8) -> ParamCoun
     head = 2 * arch.patch_volume * latent_channels * arch.hidden_size
     return ParamCountEstimate(total=float(blocks + adaln + head), transformer=float(blocks), adaln=float(adaln),
                               embedding_head=float(head))
+
+
+def resolved_param_count(arch: ModelArch) -> float:
+    """The supplied ``param_count`` when present, the estimate otherwise (``config.py:252-256``)."""
+    if arch.param_count is not None:
+        return float(arch.param_count)
+    return estimate_param_count(arch).total
 
 
 def flops_per_microstep(arch: ModelArch, B: int, S: int) -> float:
@@ -214,3 +223,29 @@ BUILTIN_CHUNKS = ChunkTable(chunks=(
     ChunkSpec("layernorm_scale_shift", coeff_bsh=4, fwd_latency_ms=0.58),
     ChunkSpec("gelu", coeff_bsh=8, fwd_latency_ms=0.64),
 ))
+
+
+_CHUNK_KEYS = ("name", "coeff_bsh", "coeff_bas", "fwd_latency_ms", "recomputable", "offloadable")
+_TABLE_META = ("ref_batch", "ref_seqlen", "ref_hidden", "ref_heads", "ref_tp")
+
+
+def load_chunk_table(path) -> ChunkTable:
+    """A :class:`ChunkTable` from a JSON file ``{"chunks": [{name, coeff_bsh, ...}], ref_*...}``
+    (``memory.py:110-134``): same accepted keys, same ``ConfigError`` messages and paths."""
+    try:
+        doc = json.loads(Path(path).read_text())
+    except OSError as exc:
+        raise ConfigError(f"cannot read chunk table: {exc}", str(path)) from exc
+    except json.JSONDecodeError as exc:
+        raise ConfigError(f"invalid JSON: {exc}", str(path)) from exc
+    if not isinstance(doc, dict) or "chunks" not in doc:
+        raise ConfigError("expected an object with a 'chunks' array", str(path))
+    chunks = []
+    for i, entry in enumerate(doc["chunks"]):
+        if not isinstance(entry, dict) or "name" not in entry:
+            raise ConfigError("chunk entry needs a name", f"chunks[{i}]")
+        extra = sorted(set(entry) - set(_CHUNK_KEYS))
+        if extra:
+            raise ConfigError("unknown key", f"chunks[{i}].{extra[0]}")
+        chunks.append(ChunkSpec(**entry))
+    return ChunkTable(chunks=tuple(chunks), **{k: doc[k] for k in _TABLE_META if k in doc})

@@ -35,29 +35,41 @@ class DenoiseResult:
 
 
 class _Graphs:
+    """One CUDA graph per (model context, step kind, cache policy) — replayed for every step."""
+
     def __init__(self):
         self.g = {}
 
+    @staticmethod
+    def key(model, mode, use_cache):
+        # the policy's threshold / warmup / force_last are baked into the captured
+        # cache_decide launch, so key on the (frozen, hashable) policy value, not its id
+        return (id(model), model.generation, mode, use_cache, model.policy, model.cache_mode, model.n_front)
+
     def run(self, model, mode, use_cache):
-        key = (id(model), model.generation, mode, use_cache, id(model.policy), model.cache_mode)
+        key = self.key(model, mode, use_cache)
         if key not in self.g:
-            # warm the kernels' one-time attribute setup outside capture
+            state = (model.idx, model.cur, model.cstate, model.prev, model.lat, model.lat_bf, model.off,
+                     model.flags_out, model.rels_out)
+            # snapshot first, then order the warm-up stream after the snapshots: the warm-up
+            # step writes the very buffers the clones read (probe -> prev, cache_decide ->
+            # cstate/flags/rels, the Euler epilogue -> lat/idx)
+            saved = tuple(t.clone() for t in state)
             s = torch.cuda.Stream()
             s.wait_stream(torch.cuda.current_stream())
-            g = torch.cuda.CUDAGraph()
-            saved = (model.idx.clone(), model.cur.clone(), model.cstate.clone(), model.prev.clone(),
-                     model.lat.clone(), model.lat_bf.clone(), model.off.clone(), model.flags_out.clone(),
-                     model.rels_out.clone())
             with torch.cuda.stream(s):
-                model.step(mode, use_cache)  # warm-up (then state is restored)
+                model.step(mode, use_cache)  # warm the kernels' one-time setup outside capture
             torch.cuda.current_stream().wait_stream(s)
-            for dst, src in zip((model.idx, model.cur, model.cstate, model.prev, model.lat, model.lat_bf, model.off,
-                                 model.flags_out, model.rels_out), saved):
+            for dst, src in zip(state, saved):
                 dst.copy_(src)
+            g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):
                 model.step(mode, use_cache)
             self.g[key] = g
         self.g[key].replay()
+
+    def clear(self):
+        self.g.clear()
 
 
 def denoise(model, x0: torch.Tensor, num_steps: int, cache=None, trajectory: bool = False,
@@ -73,7 +85,8 @@ def denoise(model, x0: torch.Tensor, num_steps: int, cache=None, trajectory: boo
             raise ConfigError("cache must be a CacheSchedule, a RelL1Policy or None", "sampler.cache")
         if cache.total_steps != num_steps:
             raise ConfigError("schedule length != num_steps", "sampler.cache")
-    model.reset(x0, num_steps, policy=cache if dynamic else None, cache_mode=cache.mode)
+    model.reset(x0, num_steps, policy=cache if dynamic else None, cache_mode=cache.mode,
+                cached_cost_fraction=cache.cached_cost_fraction)
     use_cache = dynamic or not all(cache.per_step_full)
     traj = []
     if graph and graphs is None:
@@ -135,7 +148,8 @@ def denoise_windows(model, x0: torch.Tensor, num_steps: int, plan, cache=None, t
     x = x0.to(dev, torch.float32).contiguous().clone()
     ctxs = [model] + [model.fork() for _ in range(plan.num_clips - 1)]
     for ctx, (s0, _) in zip(ctxs, plan.clips):
-        ctx.reset(x, num_steps, policy=cache if dynamic else None, cache_mode=cache.mode, frame_offset=s0)
+        ctx.reset(x, num_steps, policy=cache if dynamic else None, cache_mode=cache.mode, frame_offset=s0,
+                  cached_cost_fraction=cache.cached_cost_fraction)
     clips = [torch.empty(cfg.latent_channels, plan.window, *x.shape[2:], device=dev) for _ in plan.clips]
     use_cache = dynamic or not all(cache.per_step_full)
     graphs = _Graphs() if graph else None

@@ -188,9 +188,31 @@ def plan_temporal_windows(n_prime: int, n: int, s: int) -> WindowPlan:
 
 
 # ----------------------------------------------------------------------------- GPU kernels
-def _ptrs(tensors, device):
-    return torch.tensor([t.data_ptr() if isinstance(t, torch.Tensor) else int(t) for t in tensors],
-                        dtype=torch.int64, device=device)
+def _check_f32(t: torch.Tensor, shape, what: str, device):
+    """The blend kernels index every tensor as a dense f32 array of ``shape`` on ``device``."""
+    if not isinstance(t, torch.Tensor):
+        raise ConfigError(f"{what} must be a tensor", what)
+    if t.dtype != torch.float32 or not t.is_cuda or t.device != device:
+        raise ConfigError(f"{what} must be float32 on {device}, got {t.dtype} on {t.device}", what)
+    if not t.is_contiguous():
+        raise ConfigError(f"{what} must be contiguous", what)
+    if tuple(t.shape) != tuple(shape):
+        raise ConfigError(f"{what} must have shape {tuple(shape)}, got {tuple(t.shape)}", what)
+
+
+def _ptrs(items, shape, what, device):
+    """Device addresses of ``items``: tensors are validated against ``shape``; plain ints are
+    documented raw device addresses (e.g. a peer rank's buffer over NVLink) and pass as is."""
+    out = []
+    for k, t in enumerate(items):
+        if isinstance(t, torch.Tensor):
+            _check_f32(t, shape, f"{what}[{k}]", device)
+            out.append(t.data_ptr())
+        elif isinstance(t, int) and t > 0:
+            out.append(int(t))
+        else:
+            raise ConfigError(f"{what}[{k}] must be an f32 CUDA tensor or a device address", what)
+    return torch.tensor(out, dtype=torch.int64, device=device)
 
 
 def blend_tiles(plan: TilePlan, tiles, out: torch.Tensor) -> torch.Tensor:
@@ -203,10 +225,14 @@ def blend_tiles(plan: TilePlan, tiles, out: torch.Tensor) -> torch.Tensor:
     """
     if len(tiles) != len(plan.tiles):
         raise ConfigError("one tensor per plan tile", "vae.tiles")
+    if not isinstance(out, torch.Tensor) or out.dim() != 4:
+        raise ConfigError("out must be an f32 CUDA tensor [C, T, H, W]", "vae.out")
     dev = out.device
+    C = out.shape[0]
+    _check_f32(out, (C, *plan.latent), "vae.out", dev)
     st = plan.starts_per_axis()
     starts = torch.tensor(st[0] + st[1] + st[2], dtype=torch.int32, device=dev)
-    ptrs = _ptrs(tiles, dev)
+    ptrs = _ptrs(tiles, (C, *plan.tiles[0].size), "vae.tiles", dev)
     ops.tile_blend(ptrs, starts, [len(a) for a in st], plan.tiles[0].size, plan.overlap, plan.latent, out)
     return out
 
@@ -258,7 +284,11 @@ def average_windows(plan: WindowPlan, clips, out: torch.Tensor) -> torch.Tensor:
     """
     if len(clips) != plan.num_clips:
         raise ConfigError("one tensor per clip", "windows.clips")
+    if not isinstance(out, torch.Tensor) or out.dim() != 4:
+        raise ConfigError("out must be an f32 CUDA tensor [C, n', H, W]", "windows.out")
     dev = out.device
+    C, _, Hh, Ww = out.shape
+    _check_f32(out, (C, plan.n_prime, Hh, Ww), "windows.out", dev)
     starts = torch.tensor([c[0] for c in plan.clips], dtype=torch.int32, device=dev)
-    ops.window_average(_ptrs(clips, dev), starts, plan.num_clips, plan.window, plan.n_prime, out)
+    ops.window_average(_ptrs(clips, (C, plan.window, Hh, Ww), "windows.clips", dev), starts, plan.num_clips, plan.window, plan.n_prime, out)
     return out

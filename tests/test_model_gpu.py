@@ -101,6 +101,45 @@ def test_graph_replay_equals_eager():
     assert torch.equal(a, b)
 
 
+def test_graph_replay_equals_eager_rel_l1_policy():
+    """CUDA-graph replay of the device-decided (rel-L1) step: same latent bits, same flags and
+    the same rel-L1 values as eager launches (the capture warm-up must not leak state)."""
+    cfg, grid = CASES["single-d128"]
+    model, orc, inp = _setup(cfg, grid)
+    _, _, probe = ref.denoise(orc, inp["x0"], 4, policy=RelL1Policy(threshold=1e9, warmup=1))
+    thr = 2.5 * sorted(probe[1:])[len(probe[1:]) // 2]
+    pol = RelL1Policy(threshold=thr, warmup=2)
+    a = denoise(model, inp["x0"], 10, pol)
+    lat_a, rel_a = a.latent.clone(), list(a.rel_l1)
+    assert 0 < a.schedule.cached_steps
+    b = denoise(model, inp["x0"], 10, pol, graph=True)
+    assert b.schedule.per_step_full == a.schedule.per_step_full
+    assert b.rel_l1 == rel_a
+    assert torch.equal(b.latent, lat_a)
+    # a second policy with another threshold must not replay the first one's graph
+    pol2 = RelL1Policy(threshold=thr * 3, warmup=2)
+    graphs = __import__("paper_2505_10584_b200.sampler", fromlist=["_Graphs"])._Graphs()
+    c1 = denoise(model, inp["x0"], 10, pol, graph=True, graphs=graphs).schedule.per_step_full
+    c2 = denoise(model, inp["x0"], 10, pol2, graph=True, graphs=graphs).schedule.per_step_full
+    e2 = denoise(model, inp["x0"], 10, pol2).schedule.per_step_full
+    assert c1 == a.schedule.per_step_full and c2 == e2
+
+
+def test_cached_cost_fraction_sets_front_blocks():
+    """A schedule with cached_cost_fraction 0.5 runs ceil(0.5·L) front blocks on cached steps
+    (the fraction the schedule's speedup is costed with), matching the oracle at that split."""
+    cfg, grid = CASES["single-d128"]
+    model, _, inp = _setup(cfg, grid)
+    for frac in (0.5, 0.25, 1.0):
+        sched = plan_cache(8, warmup=2, interval=2, cached_cost_fraction=frac)
+        res = denoise(model, inp["x0"], 8, sched, trajectory=True)
+        assert model.n_front == front_block_count(cfg.num_layers, frac)
+        orc = ref.OracleDiT(cfg, init_weights(cfg, seed=0), inp["text"], None, grid,
+                            n_front=front_block_count(cfg.num_layers, frac))
+        lat, _, _ = ref.denoise(orc, inp["x0"], 8, flags=sched.per_step_full)
+        _check_traj(res, lat)
+
+
 def test_config2_dims_two_blocks_match_oracle():
     """Single-DiT 2B dims (H=2048, 16 heads, text 256x4096) at the config-2 geometry
     (17x480x832 -> 7,800 tokens), 2 of the 28 blocks, 2 steps — the CPU oracle's bounded sample."""

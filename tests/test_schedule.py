@@ -20,7 +20,8 @@ from hypothesis import strategies as st
 from oracle import schedule_oracle as so
 from paper_2505_10584_b200 import (CACHE_MODES, DEFAULT_CACHED_COST_FRACTION, CacheSchedule, ConfigError,
                                    RelL1Policy, composite_speedup, dit_parallel_latency, front_block_count,
-                                   latent_shape, no_cache, plan_cache, token_count)
+                                   latent_shape, no_cache, plan_cache, token_count, Bucket,
+                                   video_token_count)
 from paper_2505_10584_b200.errors import DimensionError, PlanningError
 
 GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "plan_cache.json")))
@@ -115,7 +116,8 @@ def test_geometry_golden():
     for case in GOLD["geometry"]:
         f, h, w = case["video"]
         assert list(latent_shape(f, h, w)) == case["latent"]
-        assert token_count(f, h, w) == case["tokens"]
+        assert video_token_count(f, h, w) == case["tokens"]
+        assert token_count(Bucket(1, f, h, w)).tokens == case["tokens"]
     with pytest.raises(DimensionError):
         latent_shape(18, 480, 832)
     with pytest.raises(DimensionError):

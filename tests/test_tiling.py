@@ -158,3 +158,44 @@ def test_peer_tiles_single_rank_blend_equals_local_blend():
         pt.close()
     finally:
         dist.destroy_process_group()
+
+
+def test_blend_and_average_validate_tensors_on_cpu():
+    """Host-side validation fires before any launch: CPU tensors are rejected (no CPU path)."""
+    plan = plan_vae_tiles((6, 20, 20), (4, 9, 9), (3, 8, 8), devices=1)
+    with pytest.raises(ConfigError):
+        blend_tiles(plan, [torch.zeros(3, *t.size) for t in plan.tiles], torch.zeros(3, *plan.latent))
+    wp = plan_temporal_windows(8, 4, 2)
+    with pytest.raises(ConfigError):
+        average_windows(wp, [torch.zeros(2, 4, 3, 3) for _ in wp.clips], torch.zeros(2, 8, 3, 3))
+
+
+@pytest.mark.gpu
+def test_blend_and_average_reject_bad_layouts():
+    """bf16 / non-contiguous / wrong-shape tiles and a sliced ``out`` raise instead of
+    reading out of bounds (the kernels index dense f32 arrays)."""
+    plan = plan_vae_tiles((6, 20, 20), (4, 9, 9), (3, 8, 8), devices=1)
+    C = 3
+    good = [torch.zeros(C, *t.size, device="cuda") for t in plan.tiles]
+    out = torch.zeros(C, *plan.latent, device="cuda")
+    blend_tiles(plan, good, out)
+    bad_dtype = [t.to(torch.bfloat16) for t in good]
+    bad_layout = [torch.zeros(C, t.size[2], t.size[1], t.size[0], device="cuda").permute(0, 3, 2, 1)
+                  for t in plan.tiles]
+    bad_shape = [torch.zeros(C + 1, *t.size, device="cuda") for t in plan.tiles]
+    for tiles in (bad_dtype, bad_layout, bad_shape):
+        with pytest.raises(ConfigError):
+            blend_tiles(plan, tiles, out)
+    wide = torch.zeros(C, plan.latent[0], plan.latent[1], plan.latent[2] + 4, device="cuda")
+    with pytest.raises(ConfigError):
+        blend_tiles(plan, good, wide[..., :plan.latent[2]])
+    with pytest.raises(ConfigError):
+        blend_tiles(plan, good, torch.zeros(C, *plan.latent, device="cuda", dtype=torch.float64))
+    wp = plan_temporal_windows(8, 4, 2)
+    clips = [torch.zeros(2, 4, 3, 3, device="cuda") for _ in wp.clips]
+    avg = torch.zeros(2, 8, 3, 3, device="cuda")
+    average_windows(wp, clips, avg)
+    with pytest.raises(ConfigError):
+        average_windows(wp, [c.to(torch.bfloat16) for c in clips], avg)
+    with pytest.raises(ConfigError):
+        average_windows(wp, clips, torch.zeros(2, 8, 3, 6, device="cuda")[..., :3])
