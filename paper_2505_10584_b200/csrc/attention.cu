@@ -691,11 +691,8 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
   }
   auto kern = poly == 0 ? attn_fwd_kernel<D, 0x00> : poly == 2 ? attn_fwd_kernel<D, 0x22>
                        : poly == 4 ? attn_fwd_kernel<D, 0x55> : attn_fwd_kernel<D, kPolyMaskDefault>;
-  static bool configured = false;
-  if (!configured) {
-    AQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  static FuncAttrOnce attr[4];  // one per exp2-split variant; per device inside
+  AQB_CUDA_TRY(set_smem_once(attr[poly == 0 ? 0 : poly == 2 ? 1 : poly == 4 ? 2 : 3], kern, smem));
   OutMaps om;
   if (p.n_whole > 0) {
     int rc = make_out_maps(p, om);

@@ -556,6 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __nv_bfloat16* sb = reinterpret_cast<__nv_bfloat16*>(base + STAGES * BM * BK * 2);
   uint8_t* ebuf = base + STAGES * (BM + BN) * BK * 2;
   constexpr int NB = epi_bufs<BN, STAGES, false, EPI>();
+  static_assert(EPI != AQB_EPI_GATE_RES || NB >= 3, "gate*residual needs >= 3 residual buffers (NB - 2 prefetch)");
   uint64_t* full = reinterpret_cast<uint64_t*>(ebuf + NB * kEpiBuf + aux_bytes<EPI>());
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
@@ -679,6 +680,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   uint8_t* sb = base + STAGES * kABytes;
   uint8_t* ebuf = base + STAGES * (kABytes + kBBytes);
   constexpr int NB = epi_bufs<BN, STAGES, true, EPI>();
+  static_assert(EPI != AQB_EPI_GATE_RES || NB >= 3, "gate*residual needs >= 3 residual buffers (NB - 2 prefetch)");
   uint8_t* rope_buf = ebuf + NB * kEpiBuf + aux_bytes<EPI>();  // rope_bytes<EPI, true>() (QK-norm only)
   uint64_t* full = reinterpret_cast<uint64_t*>(rope_buf + rope_bytes<EPI, true>());
   uint64_t* empty = full + STAGES;
@@ -820,12 +822,14 @@ int launch(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& to, 
            cudaStream_t stream) {
   constexpr int smem = smem_bytes<BN, STAGES, PAIR, EPI>();
   static_assert(smem <= 232448, "shared memory budget");
-  auto kern = PAIR ? gemm2_kernel<BN, STAGES, EPI> : gemm_kernel<BN, STAGES, EPI>;
-  static bool configured = false;  // per instantiation; the attribute is per function
-  if (!configured) {
-    AQB_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    configured = true;
-  }
+  // select at compile time: only the variant that runs is instantiated (a pair variant's
+  // stage count need not leave room for the single-CTA kernel's buffers)
+  auto kern = [] {
+    if constexpr (PAIR) return gemm2_kernel<BN, STAGES, EPI>;
+    else return gemm_kernel<BN, STAGES, EPI>;
+  }();
+  static FuncAttrOnce attr;  // per instantiation; the attribute is per function and per device
+  AQB_CUDA_TRY(set_smem_once(attr, kern, smem));
   int grid;
   if (PAIR) {
     const int pairs = sm_count() / 2;
@@ -846,7 +850,13 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
   switch (epi) {
     case AQB_EPI_BF16: return launch<BN, STAGES, AQB_EPI_BF16, PAIR>(ta, tb, to, pm, p, s);
     case AQB_EPI_GELU_BF16: return launch<BN, STAGES, AQB_EPI_GELU_BF16, PAIR>(ta, tb, to, pm, p, s);
-    case AQB_EPI_GATE_RES: return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, pm, p, s);
+    case AQB_EPI_GATE_RES:
+      // the residual-reading epilogue needs >= 3 residual buffers (it requests NB-2 chunks
+      // ahead); variants whose shared memory cannot hold them are never instantiated
+      if constexpr (epi_bufs<BN, kResStages, PAIR, AQB_EPI_GATE_RES>() >= 3)
+        return launch<BN, kResStages, AQB_EPI_GATE_RES, PAIR>(ta, tb, to, pm, p, s);
+      else
+        return set_error(AQB_EINVAL, "gate*residual epilogue does not fit variant BN=%d pair=%d", BN, int(PAIR));
     case AQB_EPI_F32: return launch<BN, STAGES, AQB_EPI_F32, PAIR>(ta, tb, to, pm, p, s);
     case kEpiGateAdd: return launch<BN, STAGES, kEpiGateAdd, PAIR>(ta, tb, to, pm, p, s);
     case kEpiGateAddScatter: return launch<BN, STAGES, kEpiGateAddScatter, PAIR>(ta, tb, to, pm, p, s);

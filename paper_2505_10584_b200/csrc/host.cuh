@@ -8,6 +8,7 @@
 #include <stdint.h>
 #include <stdio.h>
 
+#include <atomic>
 #include <cstdarg>
 #include <mutex>
 #include <utility>
@@ -60,6 +61,25 @@ cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t sme
   cfg.attrs = attr;
   cfg.numAttrs = pdl_enabled() ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel *and device*: the
+// attribute is per-device state, so a process driving several GPUs must set it on each.
+// Lock-free and reentrant (a race just repeats the idempotent call).
+struct FuncAttrOnce {
+  std::atomic<uint64_t> devices{0};  // bit d: set on device d
+};
+
+template <typename K>
+cudaError_t set_smem_once(FuncAttrOnce& once, K kern, int smem) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  const uint64_t bit = 1ull << (dev & 63);
+  if (once.devices.load(std::memory_order_acquire) & bit) return cudaSuccess;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) once.devices.fetch_or(bit, std::memory_order_release);
+  return e;
 }
 
 // Encode a bf16 tensor map with 128B swizzle.  dims/strides innermost first;

@@ -494,8 +494,6 @@ class DiTModel:
             raise ConfigError("call prepare() first", "model")
         if cache_mode not in ("dit-layer-cache", "attention-cache"):
             raise ConfigError("unknown cache mode", "cache.mode")
-        if cache_mode == "attention-cache" and self._tp():
-            raise ConfigError("attention-cache mode is not implemented under TP-SP", "cache.mode")
         self.cache_mode = cache_mode
         if cached_cost_fraction is not None:
             self.n_front = front_block_count(cfg.num_layers, cached_cost_fraction)
@@ -701,7 +699,26 @@ class _TensorParallel:
         torch.cuda.empty_cache()
 
     def _bind_attention_output(self, i):
-        pass  # TP-SP keeps its own full-sequence, local-head buffers (no attention cache)
+        """Block i's local-head attention outputs (full sequence): the shared buffers, or under
+        ``attention-cache`` block i's slots, which a cached step feeds to the row-parallel
+        projections instead of recomputing QKV + attention."""
+        if self.cache_mode == "attention-cache":
+            self._o_tp = self.ocache[i]
+            self._xo_tp = self.xocache[i] if self.xocache is not None else None
+        else:
+            self._o_tp = self.o_full
+            self._xo_tp = getattr(self, "xo_full", None)
+
+    def _alloc_attention_cache(self):
+        """Per-block slots of this rank's heads over the full sequence: [L, S_v + S_t, A/P·D]
+        (+ Single-DiT cross-attention [L, S_v, A/P·D]); rank-local, no peer memory."""
+        if self.ocache is not None:
+            return
+        cfg, g, L = self.cfg, self.geo, self.cfg.num_layers
+        hd = self.hl * cfg.head_dim
+        self.ocache = torch.zeros(L, g.Sv + g.St, hd, device=self.device, dtype=BF16)
+        if cfg.family == "single-dit":
+            self.xocache = torch.zeros(L, g.Sv, hd, device=self.device, dtype=BF16)
 
     def _rs(self, a, name, gate, flag, run_if, barrier=True):
         """Row-parallel projection of video rows: this rank's partial reduce-added into the
@@ -782,23 +799,29 @@ class SingleDiTTP(_TensorParallel, SingleDiT):
         p = f"blocks.{i}"
         mods = self._mod(i)
         S = g.Sv
+        askip, aflag, arun = ag  # attention-cache: skip (static) / gate (dynamic) the attention parts
         # self-attention: local heads over the whole sequence
-        self._ag(mods[0], mods[1], 0, flag, run_if, probe=probe)
-        ops.gemm_qknorm_rope(self.mg, W[f"{p}.qkv.w"], self.qkv_full, hd, 2, W[f"{p}.q_norm"], W[f"{p}.k_norm"], eps,
-                             bias=W[f"{p}.qkv.b"], cos=self.cos, sin=self.sin, rope_row0=0, rope_rows=S,
-                             run_flag=flag, run_if=run_if)
-        q = self.qkv_full
-        ops.attention(q, q[:, hd:], q[:, 2 * hd:], self.o_full, hl, D, workspace=self.attn_ws, run_flag=flag,
-                      run_if=run_if)
-        self._rs(self.o_full, f"{p}.proj", mods[2], flag, run_if)
+        if probe:
+            self._ag(mods[0], mods[1], 0, flag, run_if, probe=True)
+        elif not askip:
+            self._ag(mods[0], mods[1], 0, aflag, arun)
+        if not askip:
+            ops.gemm_qknorm_rope(self.mg, W[f"{p}.qkv.w"], self.qkv_full, hd, 2, W[f"{p}.q_norm"], W[f"{p}.k_norm"],
+                                 eps, bias=W[f"{p}.qkv.b"], cos=self.cos, sin=self.sin, rope_row0=0, rope_rows=S,
+                                 run_flag=aflag, run_if=arun)
+            q = self.qkv_full
+            ops.attention(q, q[:, hd:], q[:, 2 * hd:], self._o_tp, hl, D, workspace=self.attn_ws, run_flag=aflag,
+                          run_if=arun)
+        self._rs(self._o_tp, f"{p}.proj", mods[2], flag, run_if)
         # cross-attention to the text (no norm before it, PixArt-alpha): gather bf16(x)
-        self._ag(None, None, 2, flag, run_if)
-        ops.gemm_qknorm_rope(self.mg, W[f"{p}.xq.w"], self.xq_full, hd, 1, W[f"{p}.xq_norm"], None, eps,
-                             bias=W[f"{p}.xq.b"], run_flag=flag, run_if=run_if)
-        kv = self.text_kv[i]
-        ops.attention(self.xq_full, kv, kv[:, hd:], self.xo_full, hl, D, workspace=self.attn_ws, run_flag=flag,
-                      run_if=run_if)
-        self._rs(self.xo_full, f"{p}.xproj", None, flag, run_if)
+        if not askip:
+            self._ag(None, None, 2, aflag, arun)
+            ops.gemm_qknorm_rope(self.mg, W[f"{p}.xq.w"], self.xq_full, hd, 1, W[f"{p}.xq_norm"], None, eps,
+                                 bias=W[f"{p}.xq.b"], run_flag=aflag, run_if=arun)
+            kv = self.text_kv[i]
+            ops.attention(self.xq_full, kv, kv[:, hd:], self._xo_tp, hl, D, workspace=self.attn_ws, run_flag=aflag,
+                          run_if=arun)
+        self._rs(self._xo_tp, f"{p}.xproj", None, flag, run_if)
         # MLP: F/P hidden columns per rank
         self._ag(mods[3], mods[4], 0, flag, run_if)
         ops.gemm(self.mg, W[f"{p}.fc1.w"], self.h_full, bias=W[f"{p}.fc1.b"], epilogue="gelu", run_flag=flag,
@@ -836,28 +859,33 @@ class MMDiTTP(_TensorParallel, MMDiT):
         ops.gemm(a, W[f"{name}.w"], self.tpart, bias=W[f"{name}.b"], epilogue="f32", run_flag=flag, run_if=run_if)
         ops.gate_bcast(self.tpart, gate, self.tslot_dst, self.cfg.hidden_size, run_flag=flag, run_if=run_if)
 
-    def _tp_block(self, pv, pt, mv, mt, flag, run_if, probe):
+    def _tp_block(self, pv, pt, mv, mt, flag, run_if, probe, ag):
         cfg, g, W = self.cfg, self.geo, self.W
         D, eps, hl = cfg.head_dim, cfg.qk_norm_eps, self.hl
         hd = hl * D
         S, n = g.Sv, g.Sv_loc
+        askip, aflag, arun = ag  # attention-cache: skip (static) / gate (dynamic) the attention part
         # joint attention over video + text rows, local heads
-        self._ag(mv[0], mv[1], 0, flag, run_if, probe=probe, local=(mt[0], mt[1]))
-        if pv == pt:
-            ops.gemm_qknorm_rope(self.mg, W[f"{pv}.qkv.w"], self.qkv_full, hd, 2, W[f"{pv}.q_norm"],
-                                 W[f"{pv}.k_norm"], eps, bias=W[f"{pv}.qkv.b"], cos=self.cos, sin=self.sin,
-                                 rope_row0=0, rope_rows=S, run_flag=flag, run_if=run_if)
-        else:
-            ops.gemm_qknorm_rope(self.mg[:S], W[f"{pv}.qkv.w"], self.qkv_full[:S], hd, 2, W[f"{pv}.q_norm"],
-                                 W[f"{pv}.k_norm"], eps, bias=W[f"{pv}.qkv.b"], cos=self.cos, sin=self.sin,
-                                 rope_row0=0, rope_rows=S, run_flag=flag, run_if=run_if)
-            ops.gemm_qknorm_rope(self.mg[S:], W[f"{pt}.qkv.w"], self.qkv_full[S:], hd, 2, W[f"{pt}.q_norm"],
-                                 W[f"{pt}.k_norm"], eps, bias=W[f"{pt}.qkv.b"], run_flag=flag, run_if=run_if)
-        q = self.qkv_full
-        ops.attention(q, q[:, hd:], q[:, 2 * hd:], self.o_full, hl, D, workspace=self.attn_ws, run_flag=flag,
-                      run_if=run_if)
-        self._rs(self.o_full[:S], f"{pv}.proj", mv[2], flag, run_if, barrier=False)
-        self._text_rs(self.o_full[S:], f"{pt}.proj", mt[2], flag, run_if)
+        if probe:
+            self._ag(mv[0], mv[1], 0, flag, run_if, probe=True, local=(mt[0], mt[1]))
+        elif not askip:
+            self._ag(mv[0], mv[1], 0, aflag, arun, local=(mt[0], mt[1]))
+        if not askip:
+            if pv == pt:
+                ops.gemm_qknorm_rope(self.mg, W[f"{pv}.qkv.w"], self.qkv_full, hd, 2, W[f"{pv}.q_norm"],
+                                     W[f"{pv}.k_norm"], eps, bias=W[f"{pv}.qkv.b"], cos=self.cos, sin=self.sin,
+                                     rope_row0=0, rope_rows=S, run_flag=aflag, run_if=arun)
+            else:
+                ops.gemm_qknorm_rope(self.mg[:S], W[f"{pv}.qkv.w"], self.qkv_full[:S], hd, 2, W[f"{pv}.q_norm"],
+                                     W[f"{pv}.k_norm"], eps, bias=W[f"{pv}.qkv.b"], cos=self.cos, sin=self.sin,
+                                     rope_row0=0, rope_rows=S, run_flag=aflag, run_if=arun)
+                ops.gemm_qknorm_rope(self.mg[S:], W[f"{pt}.qkv.w"], self.qkv_full[S:], hd, 2, W[f"{pt}.q_norm"],
+                                     W[f"{pt}.k_norm"], eps, bias=W[f"{pt}.qkv.b"], run_flag=aflag, run_if=arun)
+            q = self.qkv_full
+            ops.attention(q, q[:, hd:], q[:, 2 * hd:], self._o_tp, hl, D, workspace=self.attn_ws, run_flag=aflag,
+                          run_if=arun)
+        self._rs(self._o_tp[:S], f"{pv}.proj", mv[2], flag, run_if, barrier=False)
+        self._text_rs(self._o_tp[S:], f"{pt}.proj", mt[2], flag, run_if)
         self._barrier(flag, run_if)
         ops.sum_slots(self.x[n:], self.tslot, run_flag=flag, run_if=run_if)
         # MLP
@@ -877,12 +905,12 @@ class MMDiTTP(_TensorParallel, MMDiT):
 
     def _mm_dual_block(self, i, flag, run_if, probe, ag):
         pi, pt = f"dual.{i}.img", f"dual.{i}.txt"
-        self._tp_block(pi, pt, self._mod(f"{pi}.mod"), self._mod(f"{pt}.mod"), flag, run_if, probe)
+        self._tp_block(pi, pt, self._mod(f"{pi}.mod"), self._mod(f"{pt}.mod"), flag, run_if, probe, ag)
 
     def _mm_single_block(self, i, flag, run_if, probe, ag):
         p = f"single.{i}"
         md = self._mod(f"{p}.mod")
-        self._tp_block(p, p, md, md, flag, run_if, probe)
+        self._tp_block(p, p, md, md, flag, run_if, probe, ag)
 
 
 def build_model(cfg: DiTConfig, **kw) -> DiTModel:

@@ -268,7 +268,7 @@ def test_temporal_multidiffusion_matches_oracle(name, n_prime, window, stride):
 def test_tp_sp_single_rank_matches_plain_model_and_oracle(family):
     """TP-SP code path (fused gather / reduce-scatter kernels, peer barriers) with P = 1 in this
     process (gloo group of one): same schedule as the plain model, within bf16 noise of it and of
-    the oracle.  Multi-rank parity: scripts/tp_check.py."""
+    the oracle.  Multi-rank parity: tests/test_multirank_gpu.py."""
     import os
     import socket
 
@@ -295,13 +295,19 @@ def test_tp_sp_single_rank_matches_plain_model_and_oracle(family):
         tp = build_model(cfg, weights=W, sp=TensorSP()).prepare(grid, inp["text"], pooled)
         plain = build_model(cfg, weights=W).prepare(grid, inp["text"], pooled)
         orc = ref.OracleDiT(cfg, W, inp["text"], pooled, grid, n_front=front_block_count(cfg.num_layers, 0.25))
-        for cache in (plan_cache(8, warmup=2, interval=2), RelL1Policy(threshold=0.06, warmup=2)):
+        _, _, probe = ref.denoise(orc, inp["x0"], 4, policy=RelL1Policy(threshold=1e9, warmup=1))
+        thr = 2.5 * sorted(probe[1:])[len(probe[1:]) // 2]
+        for cache in (plan_cache(8, warmup=2, interval=2), RelL1Policy(threshold=thr, warmup=2),
+                      plan_cache(8, warmup=2, interval=2, mode="attention-cache")):
             r_tp = denoise(tp, inp["x0"], 8, cache, trajectory=True)
             r_1 = denoise(plain, inp["x0"], 8, cache, trajectory=True)
+            o = ref.OracleDiT(cfg, W, inp["text"], pooled, grid, n_front=front_block_count(cfg.num_layers, 0.25),
+                              mode=cache.mode)
             if isinstance(cache, RelL1Policy):
-                lat, taken, _ = ref.denoise(orc, inp["x0"], 8, policy=cache)
+                lat, taken, _ = ref.denoise(o, inp["x0"], 8, policy=cache)
             else:
-                lat, taken, _ = ref.denoise(orc, inp["x0"], 8, flags=cache.per_step_full)
+                lat, taken, _ = ref.denoise(o, inp["x0"], 8, flags=cache.per_step_full)
+            assert False in taken  # every policy really caches
             assert list(r_tp.schedule.per_step_full) == list(r_1.schedule.per_step_full) == list(taken)
             assert max(rel_l2(a, b) for a, b in zip(r_tp.trajectory, r_1.trajectory)) < 5e-3
             _check_traj(r_tp, lat)
