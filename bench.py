@@ -347,11 +347,7 @@ def mmdit_720p(sp, timed, rank, video=None, workload=None, attention_cache=True)
     model.step("cached", True)
     t_full = timed(lambda: model.step("full", True), 1)
     t_cached = timed(lambda: model.step("cached", True), 1)
-    prof = ops.KernelProfiler(timing=True)
-    ops.set_profiler(prof)
-    model.step("full", True)
-    ops.set_profiler(None)
-    kinds = prof.summary()
+    kinds, method, _ = kernel_table(lambda: model.step("full", True))
     tot = sum(d["ms"] for d in kinds.values())
     n_full, n_cached = sched.full_steps, sched.cached_steps
     video_ms = n_full * t_full + n_cached * t_cached
@@ -363,6 +359,7 @@ def mmdit_720p(sp, timed, rank, video=None, workload=None, attention_cache=True)
         "value": steps / (video_ms / 1e3), "unit": "denoise_steps/s",
         "ms_full_step": t_full, "ms_cached_step": t_cached,
         "model_tflops_full_step": fl["total"] / (t_full / 1e3) / 1e12,
+        "kernel_timing": method,
         "kernels": {k: {"ms": round(v["ms"], 2), "share": round(v["ms"] / tot, 4),
                         **({"tflops": round(v["work"] / (v["ms"] / 1e3) / 1e12, 1)}
                            if k in ("gemm", "attention") else {})}
@@ -390,6 +387,76 @@ def mmdit_720p(sp, timed, rank, video=None, workload=None, attention_cache=True)
     del model
     torch.cuda.empty_cache()
     return out
+
+
+TENSOR_KINDS = ("gemm", "attention")
+
+
+def kernel_table(run):
+    """Per kind: launches, device ms and algorithmic work (FLOPs / HBM bytes) of one ``run()``.
+
+    Work comes from the launch records (``ops.KernelProfiler``); time from a CUPTI trace of a
+    second run (``ops.trace_kernels``: each kernel's own execution, PDL off).  If the tracer is
+    unavailable, CUDA events around every launch are used instead (they include launch gaps).
+    Returns (kinds, method, libaqb kernels launched)."""
+    from paper_2505_10584_b200 import ops
+
+    cnt = ops.KernelProfiler(timing=False)
+    ops.set_profiler(cnt)
+    run()
+    ops.set_profiler(None)
+    kinds = {k: dict(v) for k, v in cnt.summary().items()}
+    try:
+        tr = ops.trace_kernels(run)
+        if not tr:
+            raise RuntimeError("empty trace")
+        for k, v in tr.items():
+            d = kinds.setdefault(k, {"launches": 0, "ms": 0.0, "work": 0.0})
+            d["launches"], d["ms"] = v["launches"], v["ms"]
+        method = "CUPTI kernel durations (torch.profiler), PDL off, eager launches"
+        n = sum(v["launches"] for v in tr.values())
+    except Exception as e:  # pragma: no cover - tracer missing on the box
+        ev = ops.KernelProfiler(timing=True)
+        ops.set_profiler(ev)
+        run()
+        ops.set_profiler(None)
+        kinds = ev.summary()
+        method = f"CUDA events around every launch (tracer unavailable: {e})"
+        n = cnt.count
+    kinds = {k: v for k, v in kinds.items() if v["ms"] > 0}
+    return kinds, method, n
+
+
+def roofline(kinds):
+    """Roofline of the dominant kernel class with algorithmic work, and the per-kind table."""
+    tot_ms = sum(d["ms"] for d in kinds.values())
+    pk, pk_src = peaks()
+    dom = max((k for k in kinds if kinds[k]["work"] > 0), key=lambda k: kinds[k]["ms"])
+    d = kinds[dom]
+    if dom in TENSOR_KINDS:
+        ach = d["work"] / (d["ms"] / 1e3) / 1e12
+        peak = pk["bf16_tflops_sustained"]
+        tb, tinfo = traffic(dom)
+        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
+                "frac": ach / peak, "traffic": tb, "peak_source": f"{pk_src} bf16 sustained",
+                "share_of_step": d["ms"] / tot_ms}
+        if tinfo:
+            roof["traffic_note"] = (f"{tinfo['kernel']}: {tb / 1e6:.1f} MB DRAM per launch vs "
+                                    f"{tinfo['algorithmic_bytes_per_launch'] / 1e6:.1f} MB algorithmic ({tinfo['source']})")
+    else:
+        ach = d["work"] / (d["ms"] / 1e3) / 1e9
+        peak = pk["hbm_gbs"]
+        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
+                "traffic": None, "peak_source": f"{pk_src} hbm copy", "share_of_step": d["ms"] / tot_ms}
+    per_kind = {}
+    for k, v in sorted(kinds.items(), key=lambda kv: -kv[1]["ms"]):
+        e = {"launches": v["launches"], "ms": round(v["ms"], 3), "share": round(v["ms"] / tot_ms, 4)}
+        if k in TENSOR_KINDS and v["work"] > 0:
+            e["tflops"] = round(v["work"] / (v["ms"] / 1e3) / 1e12, 1)
+        elif v["work"] > 0:
+            e["gbs"] = round(v["work"] / (v["ms"] / 1e3) / 1e9, 1)
+        per_kind[k] = e
+    return roof, per_kind
 
 
 def run_ours(args):
@@ -477,46 +544,11 @@ def run_ours(args):
         dist.all_reduce(e2e_t, op=dist.ReduceOp.MAX)
     e2e_value = steps * args.steps / float(e2e_t)
 
-    # launch count of one video, then an instrumented (per-launch CUDA events) video
+    # per-kernel table of one video: algorithmic work per kind from the launch records,
+    # device time per kind from a CUPTI trace of the same video (PDL off)
     _log(rank, "profile")
-    cnt = ops.KernelProfiler(timing=False)
-    ops.set_profiler(cnt)
-    denoise(model, x0, steps, sched_on)
-    ops.set_profiler(None)
-    prof = ops.KernelProfiler(timing=True)
-    ops.set_profiler(prof)
-    denoise(model, x0, steps, sched_on)
-    ops.set_profiler(None)
-    kinds = prof.summary()
-    tot_ms = sum(d["ms"] for d in kinds.values())
-    pk, pk_src = peaks()
-    tensor_kinds = {"gemm", "attention"}
-    # dominant kernel class with algorithmic work (the peer barrier moves no bytes of its own)
-    dom = max((k for k in kinds if kinds[k]["work"] > 0), key=lambda k: kinds[k]["ms"])
-    d = kinds[dom]
-    if dom in tensor_kinds:
-        ach = d["work"] / (d["ms"] / 1e3) / 1e12
-        peak = pk["bf16_tflops_sustained"]
-        tb, tinfo = traffic(dom)
-        roof = {"kernel": dom, "bound": "tensor", "achieved": ach, "peak": peak, "unit": "TFLOP/s",
-                "frac": ach / peak, "traffic": tb, "peak_source": f"{pk_src} bf16 sustained",
-                "share_of_step": d["ms"] / tot_ms}
-        if tinfo:
-            roof["traffic_note"] = (f"{tinfo['kernel']}: {tb / 1e6:.1f} MB DRAM per launch vs "
-                                    f"{tinfo['algorithmic_bytes_per_launch'] / 1e6:.1f} MB algorithmic ({tinfo['source']})")
-    else:
-        ach = d["work"] / (d["ms"] / 1e3) / 1e9
-        peak = pk["hbm_gbs"]
-        roof = {"kernel": dom, "bound": "hbm", "achieved": ach, "peak": peak, "unit": "GB/s", "frac": ach / peak,
-                "traffic": None, "peak_source": f"{pk_src} hbm copy", "share_of_step": d["ms"] / tot_ms}
-    per_kind = {}
-    for k, v in sorted(kinds.items(), key=lambda kv: -kv[1]["ms"]):
-        e = {"launches": v["launches"], "ms": round(v["ms"], 3), "share": round(v["ms"] / tot_ms, 4)}
-        if k in tensor_kinds:
-            e["tflops"] = round(v["work"] / (v["ms"] / 1e3) / 1e12, 1)
-        elif v["work"] > 0:
-            e["gbs"] = round(v["work"] / (v["ms"] / 1e3) / 1e9, 1)
-        per_kind[k] = e
+    kinds, timing_method, n_kernels = kernel_table(lambda: denoise(model, x0, steps, sched_on))
+    roof, per_kind = roofline(kinds)
     attn = kinds.get("attention")
     attn_tflops = attn["work"] / (attn["ms"] / 1e3) / 1e12 if attn else None
 
@@ -560,7 +592,8 @@ def run_ours(args):
             "attention_tflops": attn_tflops,
             "model_tflops_full_step": fl["total"] / (ms_off / max(1, args.steps) / steps / 1e3) / 1e12,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": out_bytes, "d2h_bytes_per_step": out_bytes},
-            "gpu_launches": cnt.count * args.steps,
+            "gpu_launches": n_kernels * args.steps,
+            "kernel_timing": timing_method,
             "roofline": roof,
             "kernels": per_kind,
             "clocks": clocks,

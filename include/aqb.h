@@ -42,6 +42,11 @@ int aqb_abi_version(void);
 const char* aqb_build_id(void);
 const char* aqb_last_error(void);
 int aqb_sm_count(void);
+/* Programmatic dependent launch for subsequent launches of this process: 1 = on (the
+ * default unless AQB_PDL=0), 0 = off.  Returns the previous setting.  Off makes every
+ * kernel's measured duration its own execution (a PDL kernel's span includes its wait on
+ * the predecessor); the bench's per-kernel trace pass uses it. */
+int aqb_set_pdl(int on);
 
 /* ---------------------------------------------------------------------------
  * "LayerNorm + Scale/Shift" (memory.py:104):

@@ -33,13 +33,23 @@ int sm_count() {
   return cached[dev];
 }
 
+static std::atomic<int> g_pdl{-1};
+
 bool pdl_enabled() {
-  static int on = -1;
+  int on = g_pdl.load(std::memory_order_relaxed);
   if (on < 0) {
     const char* e = getenv("AQB_PDL");
-    on = (e && e[0] == '0') ? 0 : 1;
+    int want = (e && e[0] == '0') ? 0 : 1;
+    g_pdl.compare_exchange_strong(on, want);
+    on = g_pdl.load(std::memory_order_relaxed);
   }
   return on == 1;
+}
+
+int set_pdl(int on) {
+  const int prev = pdl_enabled() ? 1 : 0;
+  g_pdl.store(on ? 1 : 0, std::memory_order_relaxed);
+  return prev;
 }
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -97,5 +107,6 @@ const char* aqb_build_id(void) { return AQB_HEADER_HASH; }
 const char* aqb_last_error(void) { return aqb::last_error(); }
 
 int aqb_sm_count(void) { return aqb::sm_count(); }
+int aqb_set_pdl(int on) { return aqb::set_pdl(on); }
 
 }  // extern "C"

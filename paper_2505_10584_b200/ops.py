@@ -49,14 +49,66 @@ class KernelProfiler:
         return out
 
     def summary(self):
+        """Per kind: launches, ms (0 without timing) and algorithmic work."""
         torch.cuda.synchronize()
         out = {}
         for kind, e0, e1, work, _name in self.records:
             d = out.setdefault(kind, {"launches": 0, "ms": 0.0, "work": 0.0})
             d["launches"] += 1
-            d["ms"] += e0.elapsed_time(e1)
+            d["ms"] += e0.elapsed_time(e1) if e0 is not None else 0.0
             d["work"] += work
         return out
+
+
+# kernel symbol -> kind (the KernelProfiler kinds), for CUPTI traces of libaqb kernels
+KERNEL_KINDS = (("gemm", ("gemm",)), ("attention", ("attn_", "attention_kernel")), ("norm_modulate", ("norm_mod",)),
+                ("qk_norm_rope", ("qk_norm_rope",)), ("gemv", ("gemv",)), ("cache_offset", ("cache_offset",)),
+                ("peer", ("barrier_kernel",)),
+                ("layout", ("patchify", "heads_to_seq", "blend_kernel", "window_kernel")))
+
+
+def kernel_kind(symbol: str) -> str | None:
+    """The kind of a libaqb kernel symbol (None: not one of ours)."""
+    if "aqb::" not in symbol:
+        return None
+    for kind, keys in KERNEL_KINDS:
+        if any(k in symbol for k in keys):
+            return kind
+    return "small"
+
+
+def trace_kernels(fn) -> dict:
+    """Run ``fn`` under the CUDA activity tracer (torch.profiler / CUPTI) with programmatic
+    dependent launch off, and return per kind ``{"launches", "ms"}`` of the libaqb kernels it
+    launched — device execution time of each kernel, free of event/launch gaps (with PDL on,
+    a dependent kernel's span would include its wait for the predecessor)."""
+    from torch.profiler import ProfilerActivity, profile
+
+    prev = set_pdl(False)
+    try:
+        torch.cuda.synchronize()
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+    finally:
+        set_pdl(prev)
+    out = {}
+    for ev in prof.key_averages():
+        kind = kernel_kind(ev.key)
+        if kind is None:
+            continue
+        us = getattr(ev, "device_time_total", None)
+        if us is None:
+            us = ev.cuda_time_total
+        d = out.setdefault(kind, {"launches": 0, "ms": 0.0})
+        d["launches"] += ev.count
+        d["ms"] += us / 1e3
+    return out
+
+
+def set_pdl(on: bool) -> bool:
+    """Programmatic dependent launch on/off for subsequent launches; returns the previous state."""
+    return bool(_native.query("aqb_set_pdl", 1 if on else 0))
 
 
 _PROF: KernelProfiler | None = None
@@ -85,6 +137,7 @@ def _run(kind, work, name, *args):
     prof.count += 1
     if not prof.timing:
         _native.call(name, *args)
+        prof.records.append((kind, None, None, float(work), name))
         return
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
