@@ -176,6 +176,13 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
   // persistent over rows (grid-stride) with the next row's loads issued before this row's
   // reductions, so each CTA keeps two rows in flight
   float4 v[VPT], vn[VPT];
+  // this thread's columns are the same for every row: scale/shift stay in registers
+  float4 sc[VPT], sh[VPT];
+#pragma unroll
+  for (int j = 0; j < VPT; ++j) {
+    sc[j] = scale ? __ldg(reinterpret_cast<const float4*>(scale) + tid + T * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+    sh[j] = shift ? __ldg(reinterpret_cast<const float4*>(shift) + tid + T * j) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   int64_t row = blockIdx.x;
   if (row < rows) {
     const float4* xr = reinterpret_cast<const float4*>(x + row * ldx);
@@ -235,8 +242,6 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
     }
     rstd = rsqrtf(block_sum<NW>(ss, red) * (1.f / H) + eps);
   }
-  const float4* sh4 = reinterpret_cast<const float4*>(shift);
-  const float4* sc4 = reinterpret_cast<const float4*>(scale);
   const float nmr = -mean * rstd;
   const int64_t yoff = row * ldy;
   float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
@@ -244,9 +249,7 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
 #pragma unroll
   for (int j = 0; j < VPT; ++j) {
     const int c4 = tid + T * j;
-    const float4 sc = scale ? __ldg(sc4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 sh = shift ? __ldg(sh4 + c4) : make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4 o = modulate4(v[j], rstd, nmr, sc, sh);
+    const float4 o = modulate4(v[j], rstd, nmr, sc[j], sh[j]);
     store_outs(ys, yoff + 4 * c4, o);
     if (pr) {
       const float4 p = pr[c4];
@@ -266,122 +269,6 @@ __global__ void __launch_bounds__(NW * 32) norm_mod_row_kernel(const float* __re
   __syncthreads();  // wstat / red reused by the next row
 #pragma unroll
   for (int j = 0; j < VPT; ++j) v[j] = vn[j];
-  }
-}
-
-// Wide rows (hidden 1024..4096), the production path: warp per row, rows staged by TMA.
-// Each warp owns an R-deep ring of row buffers in shared memory; lane 0 issues a 1-D bulk
-// copy (cp.async.bulk, one instruction per row, completion on an mbarrier) R rows ahead,
-// so loads stay in flight while the warp computes — no block barriers, no per-element
-// load instructions, and the memory-level parallelism does not depend on how many rows a
-// launch has (a 975-row Ulysses shard gets every row in flight at once).  scale/shift
-// live in shared memory once per CTA.  Statistics: mean then sum of squared deviations
-// over the registers (two passes, exact), warp shuffles only.
-template <int NV>
-struct NormTma {
-  static constexpr int H = NV * 128;
-  static constexpr uint32_t kRowBytes = H * 4;
-  static constexpr int kR = 2;  // ring depth per warp
-  static constexpr int kW = (NV <= 16) ? 8 : (NV <= 24 ? 8 : 4);  // warps per CTA
-  static constexpr int kSmem = 2 * H * 4 + kW * kR * H * 4 + kW * kR * 8 + 16;
-};
-
-template <int NV, typename OutT>
-__global__ void __launch_bounds__(NormTma<NV>::kW * 32) norm_mod_tma_kernel(
-    const float* __restrict__ x, int64_t ldx, const float* __restrict__ shift, const float* __restrict__ scale,
-    const Outs<OutT> ys, int64_t ldy, int64_t rows, float eps, int kind, float* __restrict__ prev,
-    float* __restrict__ partials, const int32_t* flag, int32_t run_if) {
-  using C = NormTma<NV>;
-  constexpr int H = C::H, R = C::kR, W = C::kW;
-  extern __shared__ __align__(128) uint8_t smem_raw[];
-  float4* s_sc = reinterpret_cast<float4*>(smem_raw);
-  float4* s_sh = s_sc + H / 4;
-  float4* ring = s_sh + H / 4;  // [W][R][H/4]
-  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + W * R * (H / 4));
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float4* my_ring = ring + warp * R * (H / 4);
-  uint64_t* my_bar = bars + warp * R;
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < R; ++k) mbar_init(my_bar + k, 1);
-    fence_barrier_init();
-  }
-  pdl_wait();  // x and scale/shift (the AdaLN GEMV) are the predecessors' outputs
-  pdl_trigger();
-  if (!gate_open(flag, run_if)) return;
-  const int64_t nw = int64_t(gridDim.x) * W;
-  const int64_t r0 = int64_t(blockIdx.x) * W + warp;
-  __syncwarp();
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < R; ++k) {
-      const int64_t r = r0 + k * nw;
-      if (r < rows) {
-        mbar_arrive_expect_tx(my_bar + k, C::kRowBytes);
-        bulk_load_g2s(my_ring + k * (H / 4), x + r * ldx, C::kRowBytes, my_bar + k);
-      }
-    }
-  }
-  for (int i = threadIdx.x; i < H / 4; i += W * 32) {
-    s_sc[i] = scale ? __ldg(reinterpret_cast<const float4*>(scale) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-    s_sh[i] = shift ? __ldg(reinterpret_cast<const float4*>(shift) + i) : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
-  __syncthreads();
-  int k = 0;
-  uint32_t phase = 0;
-  for (int64_t row = r0; row < rows; row += nw) {
-    mbar_wait(my_bar + k, phase);
-    const float4* st = my_ring + k * (H / 4);
-    float4 v[NV];
-    float s = 0.f;
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      v[j] = st[lane + 32 * j];
-      s += (v[j].x + v[j].y) + (v[j].z + v[j].w);
-    }
-    // every lane has consumed the stage (s depends on all of it): refill it R rows ahead
-    __syncwarp();
-    if (lane == 0 && row + R * nw < rows) {
-      fence_proxy_async_smem();
-      mbar_arrive_expect_tx(my_bar + k, C::kRowBytes);
-      bulk_load_g2s(my_ring + k * (H / 4), x + (row + R * nw) * ldx, C::kRowBytes, my_bar + k);
-    }
-    if (++k == R) k = 0, phase ^= 1;
-    float mean = 0.f, rstd = 1.f;
-    if (kind == 0) mean = warp_sum(s) * (1.f / H);
-    if (kind != 2) {
-      float ss = 0.f;
-#pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        const float a = v[j].x - mean, b = v[j].y - mean, c = v[j].z - mean, d = v[j].w - mean;
-        ss = fmaf(a, a, ss), ss = fmaf(b, b, ss), ss = fmaf(c, c, ss), ss = fmaf(d, d, ss);
-      }
-      rstd = rsqrtf(warp_sum(ss) * (1.f / H) + eps);
-    }
-    const float nmr = -mean * rstd;
-    const int64_t yoff = row * ldy;
-    float4* pr = prev ? reinterpret_cast<float4*>(prev + row * H) : nullptr;
-    float dsum = 0.f, psum = 0.f;
-#pragma unroll
-    for (int j = 0; j < NV; ++j) {
-      const int c4 = lane + 32 * j;
-      const float4 o = modulate4(v[j], rstd, nmr, s_sc[c4], s_sh[c4]);
-      store_outs(ys, yoff + 4 * c4, o);
-      if (pr) {
-        const float4 p = pr[c4];
-        dsum += (fabsf(o.x - p.x) + fabsf(o.y - p.y)) + (fabsf(o.z - p.z) + fabsf(o.w - p.w));
-        psum += (fabsf(p.x) + fabsf(p.y)) + (fabsf(p.z) + fabsf(p.w));
-        pr[c4] = o;
-      }
-    }
-    if (pr) {
-      dsum = warp_sum(dsum);
-      psum = warp_sum(psum);
-      if (lane == 0) {
-        partials[row] = dsum;
-        partials[rows + row] = psum;
-      }
-    }
   }
 }
 
@@ -734,34 +621,6 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
     const char* e = getenv("AQB_NORM_VPT");
     vpt_env = e ? atoi(e) : 0;
     if (vpt_env != 2 && vpt_env != 4 && vpt_env != 8) vpt_env = 0;
-  }
-  static int tma_env = -1;
-  if (tma_env < 0) {
-    const char* e = getenv("AQB_NORM_TMA");
-    tma_env = (e && !strcmp(e, "0")) ? 0 : 1;
-  }
-  if (tma_env && !vpt_env && (hidden == 1024 || hidden == 2048 || hidden == 3072 || hidden == 4096) &&
-      reinterpret_cast<uintptr_t>(x) % 16 == 0) {
-#define NT_LAUNCH(NV)                                                                                           \
-  {                                                                                                             \
-    using C = NormTma<NV>;                                                                                      \
-    static FuncAttrOnce attr;                                                                                   \
-    AQB_CUDA_TRY(set_smem_once(attr, norm_mod_tma_kernel<NV, OutT>, C::kSmem));                                 \
-    const int per_sm = std::max(1, (227 * 1024) / (C::kSmem + 1024));                                           \
-    const int64_t g = std::min<int64_t>((rows + C::kW - 1) / C::kW, int64_t(sm_count()) * per_sm);             \
-    AQB_CUDA_TRY(launch_pdl(norm_mod_tma_kernel<NV, OutT>, dim3(unsigned(g)), dim3(C::kW * 32), C::kSmem, s, x, \
-                            ldx, shift, scale, yb, ldy, rows, eps, norm_kind, probe_prev, probe_partials,       \
-                            run_flag, run_if));                                                                 \
-    AQB_LAUNCH_CHECK();                                                                                         \
-    return AQB_OK;                                                                                              \
-  }
-    switch (hidden) {
-      case 1024: NT_LAUNCH(8)
-      case 2048: NT_LAUNCH(16)
-      case 3072: NT_LAUNCH(24)
-      case 4096: NT_LAUNCH(32)
-    }
-#undef NT_LAUNCH
   }
   const int vpt = vpt_env ? vpt_env : (hidden >= 3072 && hidden % 1024 == 0 ? 8 : 4);
   if (hidden >= 1024 && hidden % (128 * vpt) == 0 && hidden / (128 * vpt) >= 2 && hidden / (128 * vpt) <= 16) {

@@ -331,15 +331,6 @@ AQB_DEV void tma_store_5d(const CUtensorMap* m, const void* src, int32_t c0, int
                "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4)
                : "memory");
 }
-// 1-D bulk copy global -> this CTA's shared memory, completion counted on ``bar`` (tx bytes);
-// ``bytes`` and both addresses 16-byte aligned.  L2 policy: evict-first (read-once stream).
-AQB_DEV void bulk_load_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cta.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(kEvictFirst)
-      : "memory");
-}
 AQB_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 template <int N>
 AQB_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }

@@ -579,11 +579,15 @@ class DiTModel:
             ops.add_bcast(self.fmods, self.t0, W["final.table"])
         else:
             ops.gemv(W["t_emb.fc2.w"], self.th, self.vec, bias=W["t_emb.fc2.b"], add=self.pe, in_silu=True)
-            ops.gemv(self.mod_w, self.vec, self.allmods, bias=self.mod_b, in_silu=True)
+            self._adaln_gemv()
         n = g.Sv_loc
         ops.gemm(self.lat_bf, W["x_emb.w"], self.x[:n], bias=W["x_emb.b"], epilogue="f32")
         if g.St:
             self.x[n:].copy_(self.txt0)
+
+    def _adaln_gemv(self):
+        """Every block's AdaLN-zero modulation (MM-DiT) in one GEMV over the stacked regressors."""
+        ops.gemv(self.mod_w, self.vec, self.allmods, bias=self.mod_b, in_silu=True)
 
     def _final(self):
         cfg, W, g = self.cfg, self.W, self.geo
@@ -697,6 +701,15 @@ class _TensorParallel:
     def _tp_shard(self):
         self.W = tp_shard(self.W, self.cfg, self.sp.P, self.sp.rank)
         torch.cuda.empty_cache()
+
+    def _embed(self):
+        super()._embed()
+        if self.cache_mode == "attention-cache":
+            # a cached step's block 0 starts with a reduce-scatter into the peers' residual
+            # rows, with no all-gather (and its barrier) before it: without this barrier a
+            # rank could add into a peer's x before the peer has finished reading the last
+            # step's x (final layer) and re-embedding it (patch-embed GEMM overwrites x)
+            self._barrier()
 
     def _bind_attention_output(self, i):
         """Block i's local-head attention outputs (full sequence): the shared buffers, or under
@@ -843,14 +856,39 @@ class MMDiTTP(_TensorParallel, MMDiT):
         self._tp_setup(cfg, sp, kw)
         super().__init__(cfg, sp=sp, **kw)
         self._tp_shard()
+        # AdaLN regressors column-parallel: this rank keeps 1/P of the stacked
+        # [sum 6H, H] output rows (~4.5B parameters at 13.4B dims) and all-gathers the
+        # modulation vectors each step
+        P, r = sp.P, sp.rank
+        self.mod_rows = self.mod_w.shape[0]
+        if self.mod_rows % (4 * P):
+            raise ConfigError(f"AdaLN rows {self.mod_rows} not divisible into {P} float4 shards", "parallel.tp")
+        per = self.mod_rows // P
+        self.mod_w = self.mod_w[r * per:(r + 1) * per].contiguous()
+        self.mod_b = self.mod_b[r * per:(r + 1) * per].contiguous()
+        torch.cuda.empty_cache()
 
     def _prepare_tp(self):
         g, H = self.geo, self.cfg.hidden_size
         P, St = self.sp.P, g.St
-        e = self._tp_peer({"tslot": P * St * H * 4})
+        per = self.mod_rows // P
+        e = self._tp_peer({"tslot": P * St * H * 4, "mods": self.mod_rows * 4})
         self.tslot = self.peer.local("tslot", (P, St, H), F32)
         self.tslot_dst = self.peer.ptrs("tslot", self.sp.rank * St * H * 4)
         self.tpart = e(St, H, dt=F32)
+        self.allmods = self.peer.local("mods", (self.mod_rows,), F32)
+        self.mods_dst = self.peer.ptrs("mods", self.sp.rank * per * 4)
+        self.mods_part = e(1, per, dt=F32)
+
+    def _adaln_gemv(self):
+        """This rank's slice of the AdaLN outputs, stored into every rank's ``allmods``: the
+        all-gather of the column-parallel AdaLN Linear.  The first barrier keeps a rank from
+        overwriting a peer's vectors while the peer still reads the previous step's (its final
+        layer runs after the last block barrier); the second publishes the new ones."""
+        self._barrier()
+        ops.gemv(self.mod_w, self.vec, self.mods_part.view(-1), bias=self.mod_b, in_silu=True)
+        ops.gate_bcast(self.mods_part, None, self.mods_dst, self.mods_part.shape[1])
+        self._barrier()
 
     def _text_rs(self, a, name, gate, flag, run_if):
         """Row-parallel projection of the replicated text rows: f32 partial, gate·partial into
