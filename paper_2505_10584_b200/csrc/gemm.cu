@@ -937,9 +937,12 @@ static int pick_variant(int64_t m, int64_t n, int64_t k, bool f32_out = false) {
   // waves, K = 2048: 3900x2048x2048 44.0 -> 39.9 us, with the bf16 residual copy 50.0 ->
   // 48.0; but K = 8192 keeps the pair tiles (3900x2048x8192 99.2 vs 113.5 us;
   // `scripts/kernel_bench.py --only gemm-variants`).
+  // K = 8192 with most pairs busy keeps the pair tiles (1950x2048x8192: 52.8 vs 55.3 us in a
+  // CUDA graph, `scripts/gemm_bench.py`), a quarter-filled wave does not (975 rows: 29.6 vs 47.7).
   if (f32_out && bv == V2_256) {
     const double tiles = double((m + 255) / 256) * double((n + 255) / 256);
-    if (tiles <= sms / 2 || (tiles <= sms && k <= 4096)) bv = V2_128;
+    const bool long_k_busy = k >= 8192 && tiles > sms / 4;
+    if ((tiles <= sms / 2 && !long_k_busy) || (tiles <= sms && k <= 4096)) bv = V2_128;
   }
   return bv;
 }
@@ -1116,8 +1119,16 @@ static int qknorm_rope(const void* a, int64_t lda, const void* w, int64_t ldw, i
                    CU_TENSOR_MAP_SWIZZLE_128B);
     if (rc) return rc;
   }
-  return run(a, lda, w, ldw, m, n, k, rope_rows > 0 ? AQB_EPI_QKNORM_ROPE : kEpiQkNoRope, p, to,
-             pick_variant(m, n, k), stream, &pm);
+  // QK-norm without RoPE (cross-attention q) on a shard whose 256x256 pair tiles fill at most one
+  // wave: 128x128 single-CTA tiles overlap each tile's epilogue with the next tile's MMAs and
+  // measured fastest (1950x2048x2048: 17.6 vs 19.9 us, 975 rows: 11.0 vs 12.1; CUDA graph,
+  // `scripts/gemm_bench.py`)
+  int variant = pick_variant(m, n, k);
+  if (rope_rows == 0 && !getenv("AQB_GEMM_VARIANT") &&
+      double((m + 255) / 256) * double((n + 255) / 256) <= sm_count() / 2)
+    variant = V1_128;
+  return run(a, lda, w, ldw, m, n, k, rope_rows > 0 ? AQB_EPI_QKNORM_ROPE : kEpiQkNoRope, p, to, variant, stream,
+             &pm);
 }
 
 }  // namespace gemm
