@@ -186,6 +186,10 @@ int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const v
 int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
 /* tiles (head x 256 queries) the automatic plan runs in one pass; the rest split
  * aqb_attention_splits ways (wave-quantisation tail, or all tiles when few) */
+/* Profiling hook: device buffer (>= 64 * CTAs uint64) into which the short-KV attention kernel
+ * writes clock64 stamps of its pipeline events; NULL (default) disables.  Not thread-safe
+ * against concurrent launches; a measurement aid, off the product path. */
+int aqb_attention_trace(void* buffer);
 int aqb_attention_whole_tiles(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
 /* 256-query blocks of one head each CTA of a one-pass launch runs with K/V loaded
  * once (short KV: 2 x KV blocks fit the K/V ring, e.g. cross-attention to 256 text

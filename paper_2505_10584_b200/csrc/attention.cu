@@ -24,6 +24,7 @@
 //               1/l normalisation and TMA-staged bf16 store from the same warps.
 // TMEM: S0 | S1 | O0 | O1  (128 + 128 + D + D columns).
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -506,6 +507,340 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
+// ----------------------------------------------------------------------------
+// Short-KV attention (seq_kv <= 256, head_dim 128): the Single-DiT cross-attention to
+// the 256 text tokens.  The general kernel walks KV in 128-key blocks
+// with an online softmax, so each Q tile's QK^T -> softmax -> PV chain is serial per
+// block and only 2 blocks long — the tensor pipe idled at 33%.  Here a Q tile's whole
+// score row fits TMEM: S_t = Q_t K^T is one 128 x 256 fp32 tile (two N=128 MMAs), the
+// softmax is exact (max over all 256 keys, no rescale), P_t is packed as bf16 pairs over
+// the first 128 columns of S_t, and O_t = P_t V accumulates in the last 128 columns
+// (K = 256 from TMEM, the TS form).  A CTA owns consecutive 128-query tiles of one head
+// with K and V resident (128 KB), two TMEM slots of 256 columns ping-pong between two
+// softmax warpgroups; the epilogue frees its slot as soon as O is in registers.
+//   warp 0: TMA (K, V once; Q tiles through 2 buffers)   warp 1: MMA issuer
+//   warps 4-7 / 8-11: softmax + epilogue of even / odd tiles (thread = query row)
+struct ShortCfg {
+  static constexpr int D = 128;
+  static constexpr int kQBytes = BQ * D * 2;          // 32 KB per Q tile
+  static constexpr int kKVBlock = BKV * D * 2;        // 32 KB per 128 keys
+  static constexpr int kOffK = 0;                     // [2 key blocks][2 d-chunks][128][128 B]
+  static constexpr int kOffV = 2 * kKVBlock;
+  static constexpr int kOffQ = 4 * kKVBlock;          // [2 buffers][2 d-chunks][128][128 B]
+  static constexpr int kStage = 32 * 128;             // per softmax warp: 32 rows x 64 bf16 (128B swizzle)
+  static constexpr int kOffO = kOffQ + 2 * kQBytes;   // [8 warps][kStage]
+  static constexpr int kOffBar = kOffO + 8 * kStage;
+  static constexpr int kSmem = kOffBar + 256 + 1024;
+};
+
+struct ShortParams {
+  int seq_q, seq_kv, heads;
+  int q_tiles, tiles_per_cta, ctas_per_head;
+  float scale_log2;
+  __nv_bfloat16* o;
+  int64_t ldo, o_head_stride;
+  const int32_t* run_flag;
+  int32_t run_if;
+  // profiling hook (aqb_attention_trace): per CTA 64 clock64 stamps of the pipeline events of
+  // its first 8 tiles (MMA QK / PV issue, softmax s_full / p_full / o_ready / slot release)
+  unsigned long long* trace;
+};
+
+__device__ __forceinline__ void short_stamp(const ShortParams& p, int slot) {
+  if (p.trace != nullptr && slot < 64) p.trace[int64_t(blockIdx.x) * 64 + slot] = clock64();
+}
+
+// exp2((s - m)·c) of 32 scores (16 pairs), row-sum into acc2, packed bf16 pairs into pp[16]
+template <uint32_t kPolyMask>
+__device__ __forceinline__ void exp_pack32(const uint32_t* sr, uint64_t c2, uint64_t nm2, uint64_t (&acc2)[4],
+                                           uint32_t (&pp)[16]) {
+  const uint64_t kM = f2pack(12582912.f, 12582912.f);
+  const uint64_t kC0 = f2pack(0.99992806f, 0.99992806f), kC1 = f2pack(0.69326103f, 0.69326103f);
+  const uint64_t kC2 = f2pack(0.24261117f, 0.24261117f), kC3 = f2pack(0.05517162f, 0.05517162f);
+#pragma unroll
+  for (int pi = 0; pi < 16; ++pi) {
+    const uint64_t x2 = ffma2(f2pack(__uint_as_float(sr[2 * pi]), __uint_as_float(sr[2 * pi + 1])), c2, nm2);
+    float x0, x1, p0, p1;
+    f2unpack(x2, x0, x1);
+    if ((kPolyMask >> (pi & 7)) & 1) {
+      const uint64_t xc = f2pack(fmaxf(x0, -126.f), fmaxf(x1, -126.f));
+      const uint64_t tt = fadd2(xc, kM);
+      const uint64_t fr = fsub2(xc, fsub2(tt, kM));
+      uint64_t pq = ffma2(fr, kC3, kC2);
+      pq = ffma2(pq, fr, kC1);
+      pq = ffma2(pq, fr, kC0);
+      float q0, q1, t0, t1;
+      f2unpack(pq, q0, q1);
+      f2unpack(tt, t0, t1);
+      p0 = __uint_as_float(__float_as_uint(q0) + (__float_as_uint(t0) << 23));
+      p1 = __uint_as_float(__float_as_uint(q1) + (__float_as_uint(t1) << 23));
+    } else {
+      p0 = ex2(x0);
+      p1 = ex2(x1);
+    }
+    acc2[pi & 3] = fadd2(acc2[pi & 3], f2pack(p0, p1));
+    pp[pi] = pack_bf16(p0, p1);
+  }
+}
+
+template <uint32_t kPolyMask = kPolyMaskDefault>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_short_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                      const __grid_constant__ CUtensorMap tv, const __grid_constant__ CUtensorMap to,
+                      ShortParams p) {
+  using C = ShortCfg;
+  constexpr int D = C::D;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sK = base + C::kOffK;
+  uint8_t* sV = base + C::kOffV;
+  uint8_t* sQ = base + C::kOffQ;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + C::kOffBar);
+  uint64_t* k_full = bars;          // 1
+  uint64_t* v_full = bars + 1;      // 1
+  uint64_t* q_full = bars + 2;      // 2 (Q buffers)
+  uint64_t* q_empty = bars + 4;     // 2
+  uint64_t* s_full = bars + 6;      // 2 (TMEM slots)
+  uint64_t* p_full = bars + 8;      // 2
+  uint64_t* o_ready = bars + 10;    // 2
+  uint64_t* slot_free = bars + 12;  // 2
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 14);
+
+  const uint32_t warp = warp_idx(), lane = lane_idx();
+  const int head = blockIdx.x / p.ctas_per_head;
+  const int tile0 = (blockIdx.x % p.ctas_per_head) * p.tiles_per_cta;
+  const int ntile = min(p.tiles_per_cta, p.q_tiles - tile0);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tq);
+    tma_prefetch_desc(&tk);
+    tma_prefetch_desc(&tv);
+    tma_prefetch_desc(&to);
+    mbar_init(k_full, 1);
+    mbar_init(v_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(q_full + b, 1);
+      mbar_init(q_empty + b, 1);
+      mbar_init(s_full + b, 1);
+      mbar_init(p_full + b, 128);
+      mbar_init(o_ready + b, 1);
+      mbar_init(slot_free + b, 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 1) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  pdl_wait();
+  pdl_trigger();
+  const bool run = gate_open(p.run_flag, p.run_if) && ntile > 0;
+
+  if (!run) {
+  } else if (warp == 0) {
+    // ------------------------------------------------------------ producer
+    setmaxnreg_dec<kCtrlRegs>();
+    if (elect_one()) mbar_arrive_expect_tx(k_full, 2 * C::kKVBlock);
+    for (int kb = 0; kb < 2; ++kb)
+      for (int c = 0; c < 2; ++c)
+        if (elect_one())
+          tma_load_3d(sK + kb * C::kKVBlock + c * (BKV * 128), &tk, k_full, c * 64, head, kb * BKV, kEvictLast);
+    auto load_q = [&](int i) {
+      const int b = i & 1;
+      if (elect_one()) mbar_arrive_expect_tx(q_full + b, C::kQBytes);
+      for (int c = 0; c < 2; ++c)
+        if (elect_one())
+          tma_load_3d(sQ + b * C::kQBytes + c * (BQ * 128), &tq, q_full + b, c * 64, head, (tile0 + i) * BQ,
+                      kEvictFirst);
+    };
+    load_q(0);
+    if (elect_one()) mbar_arrive_expect_tx(v_full, 2 * C::kKVBlock);
+    for (int kb = 0; kb < 2; ++kb)
+      for (int c = 0; c < 2; ++c)
+        if (elect_one())
+          tma_load_3d(sV + kb * C::kKVBlock + c * (BKV * 128), &tv, v_full, c * 64, head, kb * BKV, kEvictLast);
+    if (ntile > 1) load_q(1);
+    for (int i = 2; i < ntile; ++i) {
+      mbar_wait(q_empty + (i & 1), ((i >> 1) - 1) & 1);  // QK^T of tile i-2 has read its buffer
+      load_q(i);
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (warp-wide, elected lane)
+    setmaxnreg_dec<kCtrlRegs>();
+    constexpr uint32_t kIdescS = idesc_bf16(BQ, BKV, 0, 0);  // Q, K both K-major
+    constexpr uint32_t kIdescO = idesc_bf16(BQ, D, 0, 1);    // P (TMEM) K-major, V MN-major
+    const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+    const uint32_t q_addr = __shfl_sync(0xffffffffu, smem_u32(sQ), 0);
+    const uint32_t k_addr = __shfl_sync(0xffffffffu, smem_u32(sK), 0);
+    const uint32_t v_addr = __shfl_sync(0xffffffffu, smem_u32(sV), 0);
+    auto qk = [&](int i) {
+      const int b = i & 1, sl = i & 1;
+      if (i >= 2) {  // slot reused: the epilogue of tile i-2 has read O out of it
+        mbar_wait(slot_free + sl, ((i >> 1) - 1) & 1);
+        tc_fence_after();
+      }
+      mbar_wait(q_full + b, (i >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0 && i < 8) short_stamp(p, i);
+      const uint32_t a0 = q_addr + b * C::kQBytes;
+#pragma unroll
+      for (int kb = 0; kb < 2; ++kb) {
+        const uint32_t b0 = k_addr + kb * C::kKVBlock;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * (BQ * 128) + (kk & 3) * 32;
+          const uint64_t da = smem_desc(a0 + off, 0, 1024), db = smem_desc(b0 + off, 0, 1024);
+          if (elect_one()) umma_bf16_ss(tm + sl * 256 + kb * 128, da, db, kIdescS, kk > 0);
+        }
+      }
+      if (elect_one()) umma_commit(s_full + sl);
+      if (elect_one()) umma_commit(q_empty + b);
+    };
+    auto pv = [&](int i) {
+      const int sl = i & 1;
+      mbar_wait(p_full + sl, (i >> 1) & 1);
+      tc_fence_after();
+      if (lane == 0 && i < 8) short_stamp(p, 8 + i);
+#pragma unroll
+      for (int kk = 0; kk < 16; ++kk) {  // 16 keys per MMA (8 packed TMEM columns of P)
+        const uint64_t db = smem_desc(v_addr + (kk >> 3) * C::kKVBlock + (kk & 7) * 16 * 128, BKV * 128, 1024);
+        if (elect_one()) umma_bf16_ts(tm + sl * 256 + 128, tm + sl * 256 + kk * 8, db, kIdescO, kk > 0);
+      }
+      if (elect_one()) umma_commit(o_ready + sl);
+    };
+    if (lane == 0) short_stamp(p, 48);
+    mbar_wait(k_full, 0);
+    tc_fence_after();
+    if (lane == 0) short_stamp(p, 49);
+    qk(0);
+    if (ntile > 1) qk(1);
+    mbar_wait(v_full, 0);
+    tc_fence_after();
+    for (int i = 0; i < ntile; ++i) {
+      pv(i);
+      if (i + 2 < ntile) qk(i + 2);
+    }
+  } else if (warp >= 4) {
+    // ------------------------------------------------------------ softmax + epilogue
+    setmaxnreg_inc<kSoftmaxRegs>();
+    const int wg = (warp - 4) / 4;  // tiles i with i % 2 == wg
+    const uint32_t quad = warp & 3;
+    const int r = quad * 32 + lane;
+    const uint32_t lane_base = (quad * 32) << 16;
+    const uint32_t s_tmem = tmem + lane_base + wg * 256;
+    const float c = p.scale_log2;
+    const uint64_t c2 = f2pack(c, c);
+    for (int i = wg; i < ntile; i += 2) {
+      const uint32_t ph = (i >> 1) & 1;
+      mbar_wait(s_full + wg, ph);
+      tc_fence_after();
+      const bool stamp = (warp & 3) == 0 && lane == 0 && i < 8;
+      if (stamp) short_stamp(p, 16 + i);
+      uint32_t sr[64];
+      // pass 1: row max over the valid keys, 64 columns at a time
+      float mx = -INFINITY;
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {
+        tmem_ld64(s_tmem + h * 64, sr);
+        tmem_wait_ld();
+        const int valid = p.seq_kv - h * 64;
+        if (valid < 64) {  // partial chunk (short text): keys past seq_kv do not count
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j >= valid) sr[j] = 0xff800000u;
+        }
+        // 8 independent 3-input max chains (FMNMX3), then a tree
+        float mm[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mm[k] = fmaxf(__uint_as_float(sr[k]), __uint_as_float(sr[k + 8]));
+#pragma unroll
+        for (int j = 16; j < 64; j += 16)
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            mm[k] = fmaxf(mm[k], fmaxf(__uint_as_float(sr[j + k]), __uint_as_float(sr[j + 8 + k])));
+        mx = fmaxf(mx, fmaxf(fmaxf(fmaxf(mm[0], mm[1]), fmaxf(mm[2], mm[3])),
+                             fmaxf(fmaxf(mm[4], mm[5]), fmaxf(mm[6], mm[7]))));
+      }
+      // pass 2: p = exp2((s - max)·c), packed bf16 pairs: keys [64h, 64h+64) -> P columns
+      // [32h, 32h+32) of the slot, i.e. over scores this thread has already read
+      const uint64_t nm2 = f2pack(-mx * c, -mx * c);
+      uint64_t acc2[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) acc2[q] = f2pack(0.f, 0.f);
+#pragma unroll 1
+      for (int h = 0; h < 4; ++h) {
+        tmem_ld64(s_tmem + h * 64, sr);
+        tmem_wait_ld();
+        const int valid = p.seq_kv - h * 64;
+        if (valid < 64) {
+#pragma unroll
+          for (int j = 0; j < 64; ++j)
+            if (j >= valid) sr[j] = 0xff800000u;  // -inf -> p = 0
+        }
+#pragma unroll
+        for (int q32 = 0; q32 < 2; ++q32) {
+          uint32_t pp[16];
+          exp_pack32<kPolyMask>(sr + 32 * q32, c2, nm2, acc2, pp);
+          tmem_st16(s_tmem + h * 32 + q32 * 16, pp);
+        }
+      }
+      float a0, a1;
+      f2unpack(fadd2(fadd2(acc2[0], acc2[1]), fadd2(acc2[2], acc2[3])), a0, a1);
+      const float l = a0 + a1;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(p_full + wg);
+      if (stamp) short_stamp(p, 24 + i);
+      // epilogue: O (columns [128, 256) of the slot) -> bf16 rows; the slot is free once read
+      mbar_wait(o_ready + wg, ph);
+      tc_fence_after();
+      if (stamp) short_stamp(p, 32 + i);
+      const float inv = l > 0.f ? 1.f / l : 0.f;
+      uint32_t u[D];  // all of O in registers first: the slot is released before the stores
+      tmem_ld64(s_tmem + 128, u);
+      tmem_ld64(s_tmem + 192, u + 64);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(slot_free + wg);
+      if (stamp) short_stamp(p, 40 + i);
+      // bf16 rows -> this warp's 128B-swizzled staging buffer (32 rows x 64 columns), one TMA
+      // store per half: coalesced, and the warp does not wait for the write to land
+      const uint32_t sbuf = smem_u32(base + C::kOffO + (warp - 4) * C::kStage) + lane * 128;
+#pragma unroll
+      for (int hf = 0; hf < 2; ++hf) {
+        if (lane == 0) bulk_wait_read<0>();  // the previous store has read the buffer
+        __syncwarp();
+#pragma unroll
+        for (int g8 = 0; g8 < 8; ++g8) {
+          const uint32_t* w = u + hf * 64 + 8 * g8;
+          st_shared_v4(sbuf + ((g8 ^ (lane & 7)) << 4),
+                       pack_bf16(__uint_as_float(w[0]) * inv, __uint_as_float(w[1]) * inv),
+                       pack_bf16(__uint_as_float(w[2]) * inv, __uint_as_float(w[3]) * inv),
+                       pack_bf16(__uint_as_float(w[4]) * inv, __uint_as_float(w[5]) * inv),
+                       pack_bf16(__uint_as_float(w[6]) * inv, __uint_as_float(w[7]) * inv));
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_3d(&to, base + C::kOffO + (warp - 4) * C::kStage, hf * 64, head,
+                       (tile0 + i) * BQ + int(quad) * 32);
+          bulk_commit();
+        }
+      }
+    }
+    if (lane == 0) bulk_wait<0>();  // stores complete before the CTA exits
+  } else {
+    setmaxnreg_dec<kCtrlRegs>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
 // Split-KV combine: one warp per row of a split tile; lane owns 4 of the D columns.
 //   O = sum_s 2^(lse_s - M) O_s / sum_s 2^(lse_s - M),  M = max_s lse_s
 __global__ void __launch_bounds__(256) attn_combine_kernel(Params p) {
@@ -714,6 +1049,89 @@ int launch(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, 
   return AQB_OK;
 }
 
+// aqb_attention_trace: device buffer the short-KV kernel stamps its pipeline events into
+static std::atomic<unsigned long long*> g_short_trace{nullptr};
+
+// Tiles per CTA of a short-KV launch: one wave of CTAs over the SMs when possible (each CTA
+// pays the K/V load once), otherwise the fewest waves.
+static void short_plan(int q_tiles, int heads, int& tpc, int& cpb) {
+  const int slots = sm_count();
+  tpc = q_tiles;
+  for (int t = 1; t <= q_tiles; ++t) {
+    const int64_t ctas = int64_t(heads) * ((q_tiles + t - 1) / t);
+    if (ctas <= slots) {
+      tpc = t;
+      break;
+    }
+  }
+  cpb = (q_tiles + tpc - 1) / tpc;
+}
+
+static int launch_short(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t ldk, int64_t khs,
+                        const void* v, int64_t ldv, int64_t vhs, int64_t seq_q, int64_t seq_kv, int heads,
+                        float scale, const OutMap& om, const int32_t* run_flag, int32_t run_if, cudaStream_t stream) {
+  constexpr int D = 128;
+  CUtensorMap tq, tk, tv;
+  const uint32_t box[3] = {64, 1, 128};
+  {
+    const uint64_t dims[3] = {D, uint64_t(heads), uint64_t(seq_q)};
+    const uint64_t str[2] = {uint64_t(qhs) * 2, uint64_t(ldq) * 2};
+    int rc = make_tmap_bf16(&tq, q, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  {
+    const uint64_t dims[3] = {D, uint64_t(heads), uint64_t(seq_kv)};
+    const uint64_t str[2] = {uint64_t(khs) * 2, uint64_t(ldk) * 2};
+    int rc = make_tmap_bf16(&tk, k, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  {
+    const uint64_t dims[3] = {D, uint64_t(heads), uint64_t(seq_kv)};
+    const uint64_t str[2] = {uint64_t(vhs) * 2, uint64_t(ldv) * 2};
+    int rc = make_tmap_bf16(&tv, v, 3, dims, str, box, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  CUtensorMap to;
+  {
+    const uint64_t dims[3] = {D, uint64_t(heads), uint64_t(seq_q)};
+    const uint64_t str[2] = {uint64_t(om.o_head_stride) * 2, uint64_t(om.ldo) * 2};
+    const uint32_t obox[3] = {64, 1, 32};
+    int rc = make_tmap_bf16(&to, om.o, 3, dims, str, obox, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (rc) return rc;
+  }
+  ShortParams p{};
+  p.seq_q = int(seq_q), p.seq_kv = int(seq_kv), p.heads = heads;
+  p.q_tiles = int((seq_q + BQ - 1) / BQ);
+  short_plan(p.q_tiles, heads, p.tiles_per_cta, p.ctas_per_head);
+  p.scale_log2 = scale * 1.4426950408889634f;
+  p.o = om.o, p.ldo = om.ldo, p.o_head_stride = om.o_head_stride;
+  p.run_flag = run_flag, p.run_if = run_if;
+  p.trace = g_short_trace.load();
+  static int poly = -1;  // AQB_ATTN_POLY: exp2 pairs (of 8) on the FMA pipe, as for the general kernel
+  if (poly < 0) {
+    const char* e = getenv("AQB_ATTN_POLY");
+    poly = (e && !strcmp(e, "0")) ? 0 : (e && !strcmp(e, "2")) ? 2 : (e && !strcmp(e, "4")) ? 4 : 3;
+  }
+  auto kern = poly == 0 ? attn_short_kernel<0x00> : poly == 2 ? attn_short_kernel<0x22>
+                       : poly == 4 ? attn_short_kernel<0x55> : attn_short_kernel<kPolyMaskDefault>;
+  static FuncAttrOnce attr[4];
+  AQB_CUDA_TRY(set_smem_once(attr[poly == 0 ? 0 : poly == 2 ? 1 : poly == 4 ? 2 : 3], kern, ShortCfg::kSmem));
+  const int64_t ctas = int64_t(heads) * p.ctas_per_head;
+  AQB_CUDA_TRY(launch_pdl(kern, dim3(unsigned(ctas)), dim3(kThreads), ShortCfg::kSmem, stream, tq, tk, tv, to, p));
+  AQB_LAUNCH_CHECK();
+  return AQB_OK;
+}
+
+// AQB_ATTN_SHORT=0 routes short KV through the general kernel (benchmarking)
+static bool short_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("AQB_ATTN_SHORT");
+    on = (e && !strcmp(e, "0")) ? 0 : 1;
+  }
+  return on == 1;
+}
+
 }  // namespace attn
 }  // namespace aqb
 
@@ -731,6 +1149,9 @@ static int run(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t l
   AQB_CHECK_ARG(ldq % 8 == 0 && ldk % 8 == 0 && ldv % 8 == 0 && om.ldo % 8 == 0, "attention: rows must be 16B aligned");
   AQB_CHECK_ARG(qhs % 8 == 0 && khs % 8 == 0 && vhs % 8 == 0 && om.o_head_stride % 8 == 0,
                 "attention: head strides must be 16B aligned");
+  if (head_dim == 128 && seq_kv <= 2 * BKV && om.nranks == 0 && kv_splits == 0 && short_enabled())
+    return launch_short(q, ldq, qhs, k, ldk, khs, v, ldv, vhs, seq_q, seq_kv, heads, softmax_scale, om, run_flag,
+                        run_if, s);
   const int nkv = int((seq_kv + BKV - 1) / BKV);
   const int64_t tiles = ((seq_q + 2 * BQ - 1) / (2 * BQ)) * heads;
   AQB_CHECK_ARG(tiles * std::min(kv_splits > 0 ? kv_splits : 16, nkv) < (1ll << 31), "attention: grid too large");
@@ -795,6 +1216,11 @@ extern "C" int aqb_attention_pairs_per_cta(int64_t seq_q, int64_t seq_kv, int32_
   if (pl.n_whole != int64_t(q_pairs) * heads) return 1;
   const int nkv = int((seq_kv + BKV - 1) / BKV);
   return choose_pairs_per_cta(q_pairs, heads, nkv, head_dim == 128 ? Cfg<128>::NS : Cfg<64>::NS);
+}
+
+extern "C" int aqb_attention_trace(void* buffer) {
+  aqb::attn::g_short_trace.store(reinterpret_cast<unsigned long long*>(buffer));
+  return AQB_OK;
 }
 
 extern "C" int aqb_attention_whole_tiles(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim) {

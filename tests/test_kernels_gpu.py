@@ -397,7 +397,7 @@ def test_attention_scatter_multi_block(g, P, rpr, St, hl, monkeypatch):
     kv = torch.randn(skv, 2, hl * d, device=dev, generator=gen).to(torch.bfloat16).view(skv, -1)
     monkeypatch.setenv("AQB_ATTN_PAIRS", "1")
     ref_o = torch.empty(sq, hl * d, device=dev, dtype=torch.bfloat16)
-    ops.attention(q, kv, kv[:, hl * d:], ref_o, hl, d)
+    ops.attention(q, kv, kv[:, hl * d:], ref_o, hl, d, splits=1)  # the general kernel, like the scatter
     monkeypatch.setenv("AQB_ATTN_PAIRS", str(g))
     outs = [torch.zeros(rpr + St, H, device=dev, dtype=torch.bfloat16) for _ in range(P)]
     rank = P - 1
