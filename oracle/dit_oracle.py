@@ -25,6 +25,8 @@ import math
 import torch
 import torch.nn.functional as F
 
+from .schedule_oracle import rel_l1_decide
+
 f32 = torch.float32
 
 
@@ -414,7 +416,9 @@ def denoise(model: OracleDiT, x0_lat: torch.Tensor, num_steps: int, flags=None, 
             # the probe (block 0's modulated input) is computed before the decision
             full_probe, _ = _probe(model, x, t)
             rel = float("nan") if m_prev is None else rel_l1(full_probe, m_prev)
-            full, acc = policy.decide(i + 1, num_steps, acc, 0.0 if m_prev is None else rel)
+            # the rule restated in the oracle (schedule_oracle.rel_l1_decide), not the product's
+            full, acc = rel_l1_decide(i + 1, num_steps, acc, 0.0 if m_prev is None else rel, policy.threshold,
+                                      policy.warmup, policy.force_last)
             rels.append(rel)
             m_prev = full_probe
             v, m0 = model.velocity(x, t, full=full, state=state)

@@ -38,3 +38,21 @@ def error_path(total_steps, warmup, interval, fraction, mode):
 def speedup(total_steps, warmup, interval, fraction):
     f = flags(total_steps, warmup, interval)
     return total_steps / sum(1.0 if x else fraction for x in f)
+
+
+def rel_l1_decide(step: int, total_steps: int, acc: float, rel: float, threshold: float, warmup: int,
+                  force_last: bool) -> tuple[bool, float]:
+    """The data-dependent cache rule (TeaCache-style; new work), restated here
+    independently of the product's ``RelL1Policy.decide`` and of its device kernel
+    (``aqb_cache_decide``): step ``s`` (1-based) is full when ``s <= max(1, warmup)``, when
+    ``force_last`` and ``s == total_steps``, or when the accumulated relative-L1 change
+    ``acc + rel`` reaches ``threshold``; a full step resets the accumulator.  Returns
+    ``(full, new_acc)``."""
+    if step <= max(1, warmup):
+        return True, 0.0
+    if force_last and step == total_steps:
+        return True, 0.0
+    acc += rel
+    if acc >= threshold:
+        return True, 0.0
+    return False, acc

@@ -160,3 +160,24 @@ def test_oracle_attention_cache_all_full_equals_no_cache():
     assert all(torch.equal(x, y) for x, y in zip(a, b))
     c, _, _ = ref.denoise(o1, inp["x0"], 3, flags=[True, False, True])
     assert not torch.equal(c[2], a[2])  # the cached step really reuses stale attention
+
+
+def test_rel_l1_rule_oracle_matches_product_policy():
+    """The oracle's independent statement of the rel-L1 cache rule and the product's
+    RelL1Policy.decide (which the device kernel aqb_cache_decide mirrors) agree on random
+    runs — the GPU tests then compare the device decisions with the oracle's."""
+    import random
+
+    from oracle.schedule_oracle import rel_l1_decide
+    from paper_2505_10584_b200 import RelL1Policy
+
+    rng = random.Random(0)
+    for _ in range(300):
+        total = rng.randint(1, 40)
+        pol = RelL1Policy(threshold=rng.uniform(0.0, 0.5), warmup=rng.randint(0, 6), force_last=rng.random() < 0.5)
+        a = b = 0.0
+        for s in range(1, total + 1):
+            rel = rng.uniform(0.0, 0.2)
+            fa, a = rel_l1_decide(s, total, a, rel, pol.threshold, pol.warmup, pol.force_last)
+            fb, b = pol.decide(s, total, b, rel)
+            assert fa == fb and a == b
