@@ -322,13 +322,15 @@ def _log(rank, msg):
 
 
 # --------------------------------------------------------------------------- our arm
-def mmdit_720p(sp, timed, rank, video=None, workload=None, attention_cache=True):
+def mmdit_720p(sp, timed, rank, video=None, workload=None, attention_cache=True, full_video=False):
     """North-star companion measurement: the 13.4B MM-DiT at BASELINE config 4's geometry
     (129x720x1280 -> 118,800 video + 256 text tokens), cache on = plan_cache(50) (24 full / 26
     cached).  One full and one cached step are timed (device events, max over ranks) after one
     warm-up of each; steps/s of the 50-step video = 50 / (24 t_full + 26 t_cached).  One more
     full step runs instrumented for the per-kernel table (joint-attention TFLOP/s).
-    ``video``/``workload``: the same measurement at another geometry (config 3, 480p)."""
+    ``video``/``workload``: the same measurement at another geometry (config 3, 480p).
+    ``full_video``: also time one complete 50-step denoise (CUDA graphs) through the public
+    ``denoise`` API — measured, not composed (config 3 by default; 720p with --mmdit-full-video)."""
     from paper_2505_10584_b200 import MM_DIT_13B, build_model, flops_per_step, ops, plan_cache
     from paper_2505_10584_b200.config import VIDEO_720P_129F
     from paper_2505_10584_b200.weights import init_weights, synthetic_inputs
@@ -368,6 +370,17 @@ def mmdit_720p(sp, timed, rank, video=None, workload=None, attention_cache=True)
     if "attention" in kinds:
         a = kinds["attention"]
         out["attention_tflops"] = a["work"] / (a["ms"] / 1e3) / 1e12
+    if full_video:
+        from paper_2505_10584_b200 import denoise
+        from paper_2505_10584_b200.sampler import _Graphs
+
+        gr = _Graphs()
+        run = lambda: denoise(model, inp["x0"], steps, sched, graph=True, graphs=gr)  # noqa: E731
+        run()  # captures the full- and the cached-step graph
+        t_video = timed(run, 1)
+        gr.clear()
+        out["measured_video"] = {"value": steps / (t_video / 1e3), "unit": "denoise_steps/s", "ms_per_video": t_video,
+                                 "note": "one complete plan_cache(50) denoise through denoise(..., graph=True)"}
     if attention_cache and not getattr(sp, "tensor_parallel", False):
         # the paper's second cache mode: every block runs, cached steps reuse each
         # block's attention output (the 86% FLOP share at 720p) — same plan_cache(50) schedule
@@ -564,10 +577,10 @@ def run_ours(args):
         torch.cuda.empty_cache()
         from paper_2505_10584_b200.config import VIDEO_480P_61F
         mm_sp = sp  # TP-SP (--parallel tp) covers both families
-        mm = mmdit_720p(mm_sp, timed, rank)
+        mm = mmdit_720p(mm_sp, timed, rank, full_video=args.mmdit_full_video)
         mm480 = mmdit_720p(mm_sp, timed, rank, VIDEO_480P_61F,
                            "config3: MM-DiT-13.4B, 61x480x848 -> 25,440 video + 256 text tokens, 50 Euler steps, "
-                           "cache on = plan_cache(50) (24 full / 26 cached)", attention_cache=False)
+                           "cache on = plan_cache(50) (24 full / 26 cached)", attention_cache=False, full_video=True)
     if mm is not None:
         peer_ok = peer_ok and mm["peer_barriers_ok"] and mm480["peer_barriers_ok"]
     # every rank: a peer barrier that timed out means a rank never arrived — the numbers are void
@@ -659,6 +672,8 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-mmdit", action="store_true", help="skip the 13.4B MM-DiT 720p companion measurement")
+    ap.add_argument("--mmdit-full-video", action="store_true",
+                    help="also time a complete 50-step 720p MM-DiT video (about 4.5 min at N=1)")
     ap.add_argument("--parallel", choices=["ulysses", "tp"], default="ulysses",
                     help="N>1: Ulysses sequence parallel (default) or TP-SP (both families)")
     args = ap.parse_args()
