@@ -91,3 +91,25 @@ def test_peer_barrier_validates_before_launch(lib_path):
     arr = _native.ptr_array([16, 32])
     assert lib.aqb_peer_barrier(arr, 2, 2, 64, None, 0, None, None, None, 1, None) == -1  # rank out of range
     assert lib.aqb_peer_barrier(arr, 0, 9, 64, None, 0, None, None, None, 1, None) == -1  # > 8 ranks
+
+
+def test_kernel_kind_mapping_of_trace_symbols():
+    """bench's CUPTI table groups libaqb kernels by symbol; foreign kernels (torch) are ignored."""
+    from paper_2505_10584_b200.ops import kernel_kind
+
+    assert kernel_kind("void aqb::gemm::gemm2_kernel<256, 4, 2>(CUtensorMap_st, ...)") == "gemm"
+    assert kernel_kind("void aqb::attn::attn_fwd_kernel<128, 82u>(CUtensorMap_st, ...)") == "attention"
+    assert kernel_kind("void aqb::attn::attn_short_kernel<82u>(CUtensorMap_st, ...)") == "attention"
+    assert kernel_kind("void aqb::attn::attn_combine_kernel(aqb::attn::Params)") == "attention"
+    assert kernel_kind("void aqb::norm_mod_row_kernel<4, 4, __nv_bfloat16>(float const*, ...)") == "norm_modulate"
+    assert kernel_kind("aqb::peer::barrier_kernel(aqb::peer::BarrierArgs)") == "peer"
+    assert kernel_kind("void aqb::step_scalars_kernel(float const*, ...)") == "small"
+    assert kernel_kind("void at::native::vectorized_elementwise_kernel<4, ...>") is None
+
+
+def test_bench_arms_share_the_config():
+    """The reference arm and ours print the same config dict (the driver compares them)."""
+    import bench
+
+    assert bench.config_dict() == bench.config_dict()
+    assert bench.config_dict()["seq_len"] == 7800
