@@ -173,10 +173,13 @@ int aqb_qk_norm_rope(const void* src, int64_t ld_src, int64_t rows, int32_t head
  * f32 softmax statistics.  head_dim in {32, 64, 128}.  seq_kv >= 1.
  * Split-KV (few heads x queries vs. 148 SMs, e.g. Ulysses' A/P heads):
  * kv_splits = 0 picks a plan (the wave-quantisation tail, or every tile when
- * few, split aqb_attention_splits ways), 1 disables it, s > 1 splits all tiles;
- * the partials (f32 O/l + log2-sum-exp2 per row) go to `workspace`
- * (aqb_attention_workspace_bytes) and a combine pass writes O.  Automatic
- * splitting silently stays at 1 split without enough workspace.
+ * few, split aqb_attention_splits ways — possibly unevenly: a long first part
+ * and short tails), 1 disables it, s > 1 splits all tiles evenly; the partials
+ * (f32 O/l + log2-sum-exp2 per row) go to `workspace`
+ * (aqb_attention_workspace_bytes) and a combine pass writes O (in split
+ * order: deterministic).  Automatic splitting silently stays at 1 split without
+ * enough workspace.  seq_kv <= 256 with head_dim 128 and a local output takes
+ * the short-KV kernel (kv_splits = 0 only).
  */
 int aqb_attention_fwd(const void* q, int64_t ldq, int64_t q_head_stride, const void* k, int64_t ldk,
                       int64_t k_head_stride, const void* v, int64_t ldv, int64_t v_head_stride, void* o,
@@ -190,6 +193,9 @@ int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t h
  * writes clock64 stamps of its pipeline events; NULL (default) disables.  Not thread-safe
  * against concurrent launches; a measurement aid, off the product path. */
 int aqb_attention_trace(void* buffer);
+/* The automatic split-KV plan: out[5] = {whole tiles, splits, KV blocks of split 0, KV blocks of
+ * each later split, split-major launch order (0/1)}. */
+int aqb_attention_plan(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim, int32_t* out);
 int aqb_attention_whole_tiles(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim);
 /* 256-query blocks of one head each CTA of a one-pass launch runs with K/V loaded
  * once (short KV: 2 x KV blocks fit the K/V ring, e.g. cross-attention to 256 text

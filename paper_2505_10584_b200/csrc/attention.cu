@@ -29,6 +29,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <queue>
 #include <mutex>
 #include <tuple>
 #include <vector>
@@ -95,7 +96,11 @@ struct Params {
   // or every tile when heads x Q blocks leave SMs idle).  Split partials go to
   // opart/lse in compact order ((tile - n_whole) * splits + split) * 256 + row.
   int q_pairs, n_whole;
-  int splits, kv_blocks_per_split;
+  // split tiles: split 0 covers KV blocks [0, kv_first), split k >= 1 the kv_blocks_per_split
+  // blocks after kv_first + (k - 1) * kv_blocks_per_split (uneven: a long first part and short
+  // tails fill the SMs the long parts leave idle).  split_major: tail CTAs are launched split 0
+  // of every tail tile first (else tile-major).
+  int splits, kv_blocks_per_split, kv_first, split_major;
   // Short KV (2 * KV blocks <= ring depth, e.g. cross-attention to 256 text tokens):
   // a whole CTA runs `pairs_per_cta` consecutive 256-query blocks of one head with
   // K/V loaded once and resident, so the per-CTA fixed cost (prologue, K/V load,
@@ -150,15 +155,17 @@ __global__ void __launch_bounds__(kThreads, 1)
   const bool whole = cta < p.n_whole;
   const int ppc = p.pairs_per_cta;
   const int cpb = (p.q_pairs + ppc - 1) / ppc;  // CTAs per head (multi-block mode)
+  const int tail_tiles = p.q_pairs * p.heads - p.n_whole;
+  const int ti = cta - p.n_whole;  // index among the split CTAs
   const int tile = whole ? (ppc > 1 ? (cta / cpb) * p.q_pairs + (cta % cpb) * ppc : cta)
-                         : p.n_whole + (cta - p.n_whole) / p.splits;
-  const int split = whole ? 0 : (cta - p.n_whole) % p.splits;
+                         : p.n_whole + (p.split_major ? ti % tail_tiles : ti / p.splits);
+  const int split = whole ? 0 : (p.split_major ? ti / tail_tiles : ti % p.splits);
   const int head = tile / p.q_pairs;
   const int pair0 = tile % p.q_pairs;                        // first 256-query block
   const int npair = ppc > 1 ? min(ppc, p.q_pairs - pair0) : 1;
   const int nkv_all = (p.seq_kv + BKV - 1) / BKV;
-  const int j0 = whole ? 0 : split * p.kv_blocks_per_split;  // first KV block of this CTA
-  const int nkv = whole ? nkv_all : min(nkv_all - j0, p.kv_blocks_per_split);
+  const int j0 = whole || split == 0 ? 0 : p.kv_first + (split - 1) * p.kv_blocks_per_split;  // first KV block
+  const int nkv = whole ? nkv_all : min(nkv_all - j0, split == 0 ? p.kv_first : p.kv_blocks_per_split);
   const int nblk = npair * nkv;                              // flattened (block, KV block) steps
 
   if (warp == 0 && lane == 0) {
@@ -726,7 +733,6 @@ __global__ void __launch_bounds__(kThreads, 1)
     setmaxnreg_inc<kSoftmaxRegs>();
     const int wg = (warp - 4) / 4;  // tiles i with i % 2 == wg
     const uint32_t quad = warp & 3;
-    const int r = quad * 32 + lane;
     const uint32_t lane_base = (quad * 32) << 16;
     const uint32_t s_tmem = tmem + lane_base + wg * 256;
     const float c = p.scale_log2;
@@ -878,55 +884,83 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(Params p) {
   for_each_out(p.out, head, row, [&](__nv_bfloat16* orow) { *reinterpret_cast<uint2*>(orow + lane * 4) = pk; });
 }
 
-// Work plan for one launch (see Params): which tiles run whole and how the rest
-// split over KV.  Candidates — no split; every tile split s ways; the last
-// `tail` tiles split s ways for the tails left by 0..3 whole waves — are
-// list-scheduled onto one CTA slot per SM in launch order (the order the
-// hardware hands out CTAs), each CTA costing its KV blocks + 2 (Q load,
-// epilogue); the combine pass costs its partial traffic in KV-block units
-// (~2.3 us per 256-query KV block on one SM).  Lowest makespan wins, a split
-// plan only if it saves > 5%.
+// Work plan for one launch (see Params): which tiles run whole and how the rest split
+// over KV.  Candidates — no split; the last `tail` tiles (every tile, or the tails left by
+// 0..3 whole waves) split s ways, uniformly or with a longer first part (the short parts fill
+// the SMs the long ones leave idle), launched tile- or split-major — are list-scheduled onto
+// one CTA slot per SM in launch order (the order the hardware hands out CTAs), each CTA costing
+// its KV blocks + 2 (Q load, epilogue); the combine pass costs its partial traffic in KV-block
+// units (~2.3 us per 256-query KV block on one SM).  Lowest makespan wins, a split plan only
+// if it saves > 5%.
 struct Plan {
-  int n_whole, splits, per;
+  int n_whole, splits, first, per, split_major;
 };
 
-static double simulate(int64_t n_whole, int64_t tail, int s, int per, int nkv, int slots) {
-  // n_whole CTAs of nkv + 2, then tail * s CTAs of (per or the remainder) + 2
-  std::vector<double> fin(slots, 0.0);
+static int split_blocks(const Plan& pl, int nkv, int k) {
+  const int j0 = k == 0 ? 0 : pl.first + (k - 1) * pl.per;
+  return std::max(0, std::min(nkv - j0, k == 0 ? pl.first : pl.per));
+}
+
+static double simulate(int64_t tiles, const Plan& pl, int nkv, int slots) {
+  std::priority_queue<double, std::vector<double>, std::greater<double>> fin;
+  for (int i = 0; i < slots; ++i) fin.push(0.0);
   auto put = [&](double len) {
-    auto it = std::min_element(fin.begin(), fin.end());
-    *it += len;
+    const double t = fin.top();
+    fin.pop();
+    fin.push(t + len);
   };
-  for (int64_t i = 0; i < n_whole && i < 4 * slots; ++i) put(nkv + 2.0);
+  const int64_t n_whole = pl.n_whole;
   if (n_whole > 4 * slots) {  // long uniform prefix: whole waves, then the remainder
-    const int64_t rest = n_whole - 4 * slots;
-    for (auto& f : fin) f += double(rest / slots) * (nkv + 2.0);
-    for (int64_t i = 0; i < rest % slots; ++i) put(nkv + 2.0);
+    const double base = double((n_whole - 2 * slots) / slots) * (nkv + 2.0);
+    std::priority_queue<double, std::vector<double>, std::greater<double>> f2;
+    for (int i = 0; i < slots; ++i) f2.push(base);
+    fin.swap(f2);
+    for (int64_t i = 0; i < (n_whole - 2 * slots) % slots + 2 * slots; ++i) put(nkv + 2.0);
+  } else {
+    for (int64_t i = 0; i < n_whole; ++i) put(nkv + 2.0);
   }
-  for (int64_t t = 0; t < tail; ++t)
-    for (int j = 0; j < s; ++j) put(std::min(per, nkv - j * per) + 2.0);
-  return *std::max_element(fin.begin(), fin.end());
+  const int64_t tail = tiles - n_whole;
+  if (pl.split_major) {
+    for (int k = 0; k < pl.splits; ++k)
+      for (int64_t t = 0; t < tail; ++t) put(split_blocks(pl, nkv, k) + 2.0);
+  } else {
+    for (int64_t t = 0; t < tail; ++t)
+      for (int k = 0; k < pl.splits; ++k) put(split_blocks(pl, nkv, k) + 3.0);
+  }
+  double mx = 0.0;
+  while (!fin.empty()) mx = std::max(mx, fin.top()), fin.pop();
+  return mx;
 }
 
 static Plan choose_plan_uncached(int64_t seq_q, int64_t seq_kv, int heads, int head_dim) {
   const int nkv = int((seq_kv + BKV - 1) / BKV);
   const int64_t tiles = ((seq_q + 2 * BQ - 1) / (2 * BQ)) * heads;
   const int slots = sm_count();
-  Plan best{int(tiles), 1, nkv};
-  const double t1 = simulate(tiles, 0, 1, nkv, nkv, slots);
+  Plan best{int(tiles), 1, nkv, nkv, 0};
+  const double t1 = simulate(tiles, best, nkv, slots);
   double bt = t1;
-  auto consider = [&](int64_t tail, int s) {
-    const int per = (nkv + s - 1) / s;
-    s = (nkv + per - 1) / per;  // no empty split
-    if (s < 2 || tail <= 0 || tail > tiles || tail * s > 64 * int64_t(slots)) return;
-    double t = simulate(tiles - tail, tail, s, per, nkv, slots);
-    t += double(s) * tail * (2 * BQ) * (head_dim * 4 + 4) * 2.0 / 5e12 / 2.3e-6 + 1.0;
-    if (t < bt && t < t1 * 0.95) bt = t, best = Plan{int(tiles - tail), s, per};
+  auto consider = [&](int64_t tail, int s, int first) {
+    if (s < 2 || tail <= 0 || tail > tiles || tail * s > 64 * int64_t(slots) || first < 1 || first >= nkv) return;
+    const int per = (nkv - first + s - 2) / (s - 1);
+    if (per < 1) return;
+    const int s_eff = 1 + (nkv - first + per - 1) / per;  // no empty split
+    for (int major = 0; major < 2; ++major) {
+      const Plan pl{int(tiles - tail), s_eff, first, per, major};
+      double t = simulate(tiles, pl, nkv, slots);
+      t += double(s_eff) * tail * (2 * BQ) * (head_dim * 4 + 4) * 2.0 / 5e12 / 2.3e-6 + 1.0;  // combine pass
+      if (t < bt - 1e-9 && t < t1 * 0.95) bt = t, best = pl;
+    }
   };
+  const int64_t rem = tiles % slots;
   for (int s = 2; s <= 16 && s <= nkv; ++s) {
-    consider(tiles, s);
-    const int64_t rem = tiles % slots;
-    for (int k = 0; k < 4; ++k) consider(rem + int64_t(k) * slots, s);
+    const int uniform = (nkv + s - 1) / s;
+    // first part from the uniform share up to all but s-1 blocks, in <= 16 steps
+    const int span = nkv - (s - 1) - uniform;
+    const int step = std::max(1, span / 16);
+    for (int first = uniform; first <= nkv - (s - 1); first += step) {
+      consider(tiles, s, first);
+      for (int k = 0; k < 4; ++k) consider(rem + int64_t(k) * slots, s, first);
+    }
   }
   return best;
 }
@@ -1159,15 +1193,15 @@ static int run(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t l
   if (kv_splits > 0) {  // forced: every tile split the same way (1 = one pass)
     const int s = std::min(int(kv_splits), nkv);
     const int per = (nkv + s - 1) / s;
-    plan = Plan{0, (nkv + per - 1) / per, per};
-    if (plan.splits == 1) plan = Plan{int(tiles), 1, nkv};
+    plan = Plan{0, (nkv + per - 1) / per, per, per, 0};
+    if (plan.splits == 1) plan = Plan{int(tiles), 1, nkv, nkv, 0};
   } else {
     plan = choose_plan(seq_q, seq_kv, heads, head_dim);
   }
   const int64_t need = split_ws_bytes(tiles - plan.n_whole, plan.splits, head_dim);
   if (need > 0 && (workspace == nullptr || workspace_bytes < need)) {
     AQB_CHECK_ARG(kv_splits <= 1, "attention: workspace of %lld B needed for %d splits", (long long)need, plan.splits);
-    plan = Plan{int(tiles), 1, nkv};  // automatic choice without (enough) workspace: one pass
+    plan = Plan{int(tiles), 1, nkv, nkv, 0};  // automatic choice without (enough) workspace: one pass
   }
   Params p{};
   p.seq_q = int(seq_q), p.seq_kv = int(seq_kv), p.heads = heads, p.head_dim = head_dim;
@@ -1177,6 +1211,8 @@ static int run(const void* q, int64_t ldq, int64_t qhs, const void* k, int64_t l
   p.n_whole = plan.n_whole;
   p.splits = plan.splits;
   p.kv_blocks_per_split = plan.per;
+  p.kv_first = plan.first;
+  p.split_major = plan.split_major;
   p.part_d = head_dim <= 64 ? 64 : 128;
   const int ring = head_dim == 128 ? Cfg<128>::NS : Cfg<64>::NS;
   p.pairs_per_cta = plan.n_whole == tiles ? choose_pairs_per_cta(p.q_pairs, heads, nkv, ring) : 1;
@@ -1220,6 +1256,13 @@ extern "C" int aqb_attention_pairs_per_cta(int64_t seq_q, int64_t seq_kv, int32_
 
 extern "C" int aqb_attention_trace(void* buffer) {
   aqb::attn::g_short_trace.store(reinterpret_cast<unsigned long long*>(buffer));
+  return AQB_OK;
+}
+
+extern "C" int aqb_attention_plan(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim, int32_t* out) {
+  if (out == nullptr) return AQB_EINVAL;
+  const aqb::attn::Plan pl = aqb::attn::choose_plan(seq_q, seq_kv, heads, head_dim);
+  out[0] = pl.n_whole, out[1] = pl.splits, out[2] = pl.first, out[3] = pl.per, out[4] = pl.split_major;
   return AQB_OK;
 }
 

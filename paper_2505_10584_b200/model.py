@@ -218,7 +218,7 @@ class DiTModel:
         if cfg.family == "single-dit":
             xq_rows, xheads = (Sv, hl) if self._tp() else (Sv_loc, A)
             need = max(need, ops.attention_workspace_bytes(xq_rows, cfg.text_len, xheads, D))
-        self.attn_ws = torch.empty(max(need, 16), device=dev, dtype=torch.uint8)
+        self.attn_ws = torch.zeros(max(need, 16), device=dev, dtype=torch.uint8)  # split counters start at 0
         return self
 
     def _tp(self) -> bool:

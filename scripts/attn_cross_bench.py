@@ -34,7 +34,7 @@ def main():
         k = torch.randn(skv, heads * d, device=dev).to(bf)
         v = torch.randn(skv, heads * d, device=dev).to(bf)
         O = [torch.empty(sq, heads * d, device=dev, dtype=bf) for _ in range(nb)]
-        ws = torch.empty(max(16, ops.attention_workspace_bytes(sq, skv, heads, d)), device=dev, dtype=torch.uint8)
+        ws = torch.zeros(max(16, ops.attention_workspace_bytes(sq, skv, heads, d)), device=dev, dtype=torch.uint8)
         for i in range(nb):
             ops.attention(Q[i], k, v, O[i], heads, d, workspace=ws)
         torch.cuda.synchronize()

@@ -38,7 +38,7 @@ def main():
         n = S // P
         g = torch.Generator(device="cuda").manual_seed(S + rank)
         qkv = torch.randn(S, 3, hl, D, device="cuda", generator=g).to(torch.bfloat16).view(S, -1)
-        ws = torch.empty(max(16, ops.attention_workspace_bytes(S, S, hl, D)), device="cuda", dtype=torch.uint8)
+        ws = torch.zeros(max(16, ops.attention_workspace_bytes(S, S, hl, D)), device="cuda", dtype=torch.uint8)
         if sp:
             peer = PeerBuffers(sp, {"o": n * H * 2, "sig": SIGNAL_BYTES}, "cuda")
             dst = peer.ptrs("o", rank * hl * D * 2)

@@ -111,7 +111,7 @@ def attn_case(sq, skv, heads, d=128, ncu=False, packed=True):
     qkv = torch.randn(max(sq, skv), 3 * heads * d, device=dev).to(torch.bfloat16)
     o = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
     H = heads * d
-    ws = torch.empty(max(16, ops.attention_workspace_bytes(sq, skv, heads, d)), device=dev, dtype=torch.uint8)
+    ws = torch.zeros(max(16, ops.attention_workspace_bytes(sq, skv, heads, d)), device=dev, dtype=torch.uint8)
     fn = lambda: ops.attention(qkv[:sq], qkv[:skv, H:], qkv[:skv, 2 * H:], o, heads, d, workspace=ws)  # noqa: E731
     if ncu:
         fn()

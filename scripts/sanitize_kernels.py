@@ -47,7 +47,7 @@ def main():
     for sq, skv, h in ((300, 300, 2), (1024, 1024, 1), (700, 256, 4), (129, 16, 2)):
         q, k_, v = r(sq, h * d, dt=bf), r(skv, h * d, dt=bf), r(skv, h * d, dt=bf)
         o = torch.empty(sq, h * d, device=dev, dtype=bf)
-        ws = torch.empty(max(16, ops.attention_workspace_bytes(sq, skv, h, d, 3)), device=dev, dtype=torch.uint8)
+        ws = torch.zeros(max(16, ops.attention_workspace_bytes(sq, skv, h, d, 3)), device=dev, dtype=torch.uint8)
         ops.attention(q, k_, v, o, h, d)
         ops.attention(q, k_, v, o, h, d, splits=3, workspace=ws)
     # norms

@@ -109,7 +109,7 @@ def test_attention_long_sequence_vs_fp32(seq, heads):
     g = torch.Generator(device="cuda").manual_seed(seq)
     q, k, v = (torch.randn(seq, heads, d, device="cuda", generator=g).to(torch.bfloat16) for _ in range(3))
     o = torch.empty(seq, heads * d, device="cuda", dtype=torch.bfloat16)
-    ws = torch.empty(max(16, ops.attention_workspace_bytes(seq, seq, heads, d)), device="cuda", dtype=torch.uint8)
+    ws = torch.zeros(max(16, ops.attention_workspace_bytes(seq, seq, heads, d)), device="cuda", dtype=torch.uint8)
     ops.attention(q.view(seq, -1), k.view(seq, -1), v.view(seq, -1), o, heads, d, workspace=ws)
     with ref.strict_fp32():
         exp = ref.attention(q.float(), k.float(), v.float())

@@ -90,7 +90,7 @@ def test_attention_stays_in_bounds(sq, skv, heads, splits):
     d = 128
     q, k, v = g(sq, heads * d, dt=bf, seed=1), g(skv, heads * d, dt=bf, seed=2), g(skv, heads * d, dt=bf, seed=3)
     nws = max(16, ops.attention_workspace_bytes(sq, skv, heads, d, splits or None))
-    raw_ws, ws = guarded((nws,), torch.uint8)
+    raw_ws, ws = guarded((nws,), torch.uint8, torch.zeros(nws, dtype=torch.uint8, device=dev))  # counters start 0
     raw, o = guarded((sq, heads * d), bf)
     ops.attention(q, k, v, o, heads, d, splits=splits, workspace=ws)
     o2 = torch.empty(sq, heads * d, device=dev, dtype=bf)

@@ -350,7 +350,7 @@ def test_attention_split_kv(sq, skv, heads, d, splits):
     v = torch.randn(skv, heads * d, device=dev, generator=g).to(torch.bfloat16)
     o1 = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
     ops.attention(q, k, v, o1, heads, d, splits=1)
-    ws = torch.empty(ops.attention_workspace_bytes(sq, skv, heads, d, splits or None), device=dev, dtype=torch.uint8)
+    ws = torch.zeros(ops.attention_workspace_bytes(sq, skv, heads, d, splits or None), device=dev, dtype=torch.uint8)
     o2 = torch.empty_like(o1)
     ops.attention(q, k, v, o2, heads, d, splits=splits, workspace=ws)
     exp = _attn_ref(q.view(sq, heads, d), k.view(skv, heads, d), v.view(skv, heads, d))
@@ -426,12 +426,38 @@ def test_attention_auto_splits_for_few_heads():
 
 def test_attention_tail_plan():
     """Config 2 (16 heads x 31 blocks of 256 queries = 496 tiles on 148 SMs): three whole waves,
-    the 52-tile tail split over KV so the last wave is not a third full."""
+    the 52-tile tail split over KV so the last wave is not a third full; a Ulysses shard of 8 or
+    4 heads (248 / 124 tiles) splits too, with a long first part and short tails that fill the SMs
+    the long parts leave idle (uneven split, merged in-kernel)."""
     from paper_2505_10584_b200 import _native
     assert _native.query("aqb_attention_whole_tiles", 7800, 7800, 16, 128) == 3 * 148
-    assert _native_splits(7800, 7800, 16, 128) == 2
-    assert _native.query("aqb_attention_whole_tiles", 7800, 7800, 8, 128) == 248  # no split pays
-    assert ops.attention_workspace_bytes(7800, 7800, 8, 128) == 0
+    assert _native_splits(7800, 7800, 16, 128) >= 2
+    assert _native.query("aqb_attention_whole_tiles", 7800, 7800, 8, 128) % 148 == 0
+    assert _native_splits(7800, 7800, 8, 128) >= 2
+    assert ops.attention_workspace_bytes(7800, 7800, 8, 128) > 0
+
+
+@pytest.mark.parametrize("heads", [16, 8, 4, 2])
+def test_attention_planned_splits_match_single_pass(heads):
+    """The planner's split (possibly uneven parts, launched split-major) equals the one-pass kernel
+    within bf16 rounding, bit-identically twice in a row, and matches fp32 attention."""
+    sq = skv = 7800
+    d = 128
+    g = torch.Generator(device=dev).manual_seed(heads)
+    q = torch.randn(sq, heads * d, device=dev, generator=g).to(torch.bfloat16)
+    k = torch.randn(skv, heads * d, device=dev, generator=g).to(torch.bfloat16)
+    v = torch.randn(skv, heads * d, device=dev, generator=g).to(torch.bfloat16)
+    ws = torch.zeros(max(16, ops.attention_workspace_bytes(sq, skv, heads, d)), device=dev, dtype=torch.uint8)
+    o1 = torch.empty(sq, heads * d, device=dev, dtype=torch.bfloat16)
+    ops.attention(q, k, v, o1, heads, d, splits=1)
+    o2, o3 = torch.empty_like(o1), torch.empty_like(o1)
+    ops.attention(q, k, v, o2, heads, d, workspace=ws)
+    ops.attention(q, k, v, o3, heads, d, workspace=ws)
+    assert torch.equal(o2, o3)
+    assert rel_l2(o2, o1) < 8e-3
+    sel = slice(0, 1000)  # fp32 reference on a row subset
+    exp = _attn_ref(q[sel].view(-1, heads, d), k.view(skv, heads, d), v.view(skv, heads, d))
+    assert rel_l2(o2[sel], exp) < 1e-2
 
 
 @pytest.mark.parametrize("splits,P,rpr,St,hl", [(1, 4, 300, 40, 2), (3, 4, 300, 40, 2), (1, 2, 192, 0, 4),
@@ -448,12 +474,12 @@ def test_attention_scatter_rows_to_owners(splits, P, rpr, St, hl):
     ref_o = torch.empty(sq, hl * d, device=dev, dtype=torch.bfloat16)
     wsb = ops.attention_workspace_bytes(sq, sq, hl, d, splits or None)
     ops.attention(flat, flat[:, hl * d:], flat[:, 2 * hl * d:], ref_o, hl, d, splits=splits,
-                  workspace=torch.empty(wsb, device=dev, dtype=torch.uint8))
+                  workspace=torch.zeros(wsb, device=dev, dtype=torch.uint8))
     outs = [torch.zeros(rpr + St, H, device=dev, dtype=torch.bfloat16) for _ in range(P)]
     rank = 1
     dst = [o.data_ptr() + rank * hl * d * 2 for o in outs]
     torch.cuda.synchronize()
-    ws = torch.empty(wsb, device=dev, dtype=torch.uint8)
+    ws = torch.zeros(wsb, device=dev, dtype=torch.uint8)
     ops.attention_scatter(flat, flat[:, hl * d:], flat[:, 2 * hl * d:], dst, H, hl, d, rpr, P * rpr, splits=splits,
                           workspace=ws)
     cols = slice(rank * hl * d, (rank + 1) * hl * d)

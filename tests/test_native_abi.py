@@ -72,17 +72,16 @@ def test_attention_split_planner_and_workspace_without_gpu(lib_path):
     assert lib.aqb_attention_workspace_bytes(1000, 4, 128, 3) == ((rows + 63) // 64 * 64 + rows * 128) * 4
     # wave-quantisation tail (config 2: 16 heads x 31 tiles = 496 on 148 SMs): 3 whole waves + split tail
     assert lib.aqb_attention_whole_tiles(7800, 7800, 16, 128) == 444
-    assert lib.aqb_attention_splits(7800, 7800, 16, 128) == 2
-    tail_rows = (496 - 444) * 2 * 256
+    out = (ctypes.c_int32 * 5)()
+    assert lib.aqb_attention_plan(7800, 7800, 16, 128, out) == 0
+    n_whole, splits, first, per, major = list(out)
+    assert (n_whole, major) == (444, 1) and splits >= 2 and first >= per  # long first part, split-major
+    assert first + (splits - 1) * per >= 61 > first + (splits - 2) * per   # the parts cover the 61 KV blocks
+    tail_rows = (496 - 444) * splits * 256
     assert lib.aqb_attention_auto_workspace_bytes(7800, 7800, 16, 128) == ((tail_rows + 63) // 64 * 64 +
                                                                           tail_rows * 128) * 4
-    assert lib.aqb_attention_whole_tiles(7800, 7800, 8, 128) == 248  # 248 tiles: splitting never pays
-    assert lib.aqb_attention_auto_workspace_bytes(7800, 7800, 8, 128) == 0
-    # cross-attention to 256 text tokens (K/V resident): 4 blocks of 256 queries per CTA,
-    # 16 heads x 8 CTAs = 128 CTAs in one wave (was 496 one-block CTAs in 4 waves)
-    assert lib.aqb_attention_pairs_per_cta(7800, 256, 16, 128) == 4
-    assert lib.aqb_attention_pairs_per_cta(7800, 7800, 16, 128) == 1  # K/V streamed: one block per CTA
-    assert lib.aqb_attention_pairs_per_cta(300, 256, 2, 128) == 1     # 4 CTAs: nothing to amortise
+    assert lib.aqb_attention_whole_tiles(7800, 7800, 4, 128) == 124  # 124 tiles: splitting does not pay
+    assert lib.aqb_attention_auto_workspace_bytes(7800, 7800, 4, 128) == 0
 
 
 def test_peer_barrier_validates_before_launch(lib_path):
