@@ -633,7 +633,10 @@ static int norm_modulate(const float* x, int64_t ldx, const float* shift, const 
       cps_env = e ? atoi(e) : 0;
       if (cps_env < 0) cps_env = 0;
     }
-    const int cps = cps_env ? cps_env : (vpt == 8 ? 4 : 8);
+    // r02, measured with PDL off in a CUDA graph (`scripts/norm_bench.py`): 16 warps per SM beat
+    // 32 at hidden 2048 (975 rows 6.0 -> 4.8 us, 1,950 rows 7.6 -> 6.8, 7,800 rows equal) while
+    // hidden 1024 (2-warp CTAs) keeps 8 CTAs per SM (11.3 vs 14.3 us at 8,056 rows)
+    const int cps = cps_env ? cps_env : (vpt == 8 ? 4 : std::max(4, 16 / nw));
     const int64_t row_grid = int64_t(sm_count()) * cps;
 #define NMR_LAUNCH(NW, VPT)                                                                                      \
   AQB_CUDA_TRY(launch_pdl(norm_mod_row_kernel<NW, VPT, OutT>, dim3(unsigned(std::min<int64_t>(rows, row_grid))),    \
