@@ -8,6 +8,8 @@ BASELINE configs can be checked end to end at their real size:
   whose threshold comes from the oracle's own probe (so it really skips);
 * config 3 — MM-DiT 13.4B, all 54 blocks (25 dual + 29 joint), 25,440 video + 256 text tokens,
   4 steps of ``plan_cache(4, 1, 2)`` (FFcF, one cached step through the 14 front blocks);
+* config 4's geometry (118,800 + 256 tokens) through one dual-stream and one joint block of the
+  13.4B dims, 4 steps with a cached one;
 * joint attention at 119,056 tokens (config 4's sequence, 3 heads = one rank's share at
   P = 8) and 131,072 tokens (config 5's longest) against fp32 softmax attention.
 
@@ -119,3 +121,26 @@ def test_attention_long_sequence_vs_fp32(seq, heads):
     # and per head, so a wrong head cannot hide behind the others
     for h in range(heads):
         assert rel_l2(o[:, h * d:(h + 1) * d], exp[:, h * d:(h + 1) * d]) <= TOL_BF16
+
+
+def test_config4_geometry_mmdit_two_blocks():
+    """Config 4's geometry — 129x720x1280 -> 118,800 video + 256 text tokens — through the 13.4B
+    MM-DiT dims (H=3072, 24 heads) with one dual-stream and one joint block, 4 steps of
+    plan_cache(4, 1, 2) = FFcF (the joint block is the rear block a cached step skips), against the fp32
+    oracle on the GPU: the joint attention over 119,056 tokens, the RoPE tables of a 33x45x80 grid
+    and the cache offset at the full size."""
+    from paper_2505_10584_b200.config import VIDEO_720P_129F, with_overrides
+    cfg = with_overrides(MM_DIT_13B, num_dual=1, num_single=1)
+    grid = VIDEO_720P_129F.grid(cfg)
+    assert grid[0] * grid[1] * grid[2] == 118_800
+    model, orc, inp = _pair(cfg, grid)
+    sched = plan_cache(4, warmup=1, interval=2)
+    assert sched.as_string() == "FFcF"
+    res = denoise(model, inp["x0"], 4, sched, trajectory=True)
+    lat, taken, _ = ref.denoise(orc, inp["x0"], 4, flags=sched.per_step_full)
+    assert tuple(taken) == res.schedule.per_step_full
+    errs = _errs(res, lat)
+    print("config4 geometry (1 dual + 1 joint block) FFcF per-step rel-L2:", ["%.2e" % e for e in errs])
+    del model, orc
+    torch.cuda.empty_cache()
+    assert max(errs) <= TOL_BF16, errs
