@@ -29,7 +29,6 @@ with a device flag — no host round-trip.
 
 from __future__ import annotations
 
-import math
 from dataclasses import dataclass
 
 import torch

@@ -5,7 +5,6 @@ same cache skip schedule.  Weights / inputs follow the synthetic contract
 (seed 0 weights, seed 1 noise, seed 2 text).
 """
 
-import math
 
 import pytest
 import torch

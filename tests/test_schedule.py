@@ -10,7 +10,6 @@ The reference's own hot-path tests (pkg/tests/test_inference.py:18-67,
 """
 
 import json
-import math
 import os
 
 import pytest
@@ -126,7 +125,6 @@ def test_geometry_golden():
 
 def test_flops_formula_golden():
     """Our per-step FLOP convention reduces to the reference's for plain joint attention."""
-    from paper_2505_10584_b200.config import DiTConfig
 
     for case in GOLD["flops_per_microstep"]:
         if case["arch"] != "TABLE2_FIT":
