@@ -1,9 +1,10 @@
 #!/usr/bin/env python
-"""Multi-GPU VAE tile blend: every rank decodes its round-robin tiles into peer memory and
-blends all of them over NVLink; vs the 1-GPU blend of the same tiles (bitwise) and the
-identity property (tiles cut from one volume blend back to it).
+"""Multi-rank VAE tile blend worker (``tests/test_multirank_gpu.py``): every rank "decodes" its
+round-robin tiles (``plan.tiles_of(rank)``, ``inference.py:189-226``) into peer memory and blends
+all of them straight from their owners' buffers (``tiling.PeerTiles``); the result must equal the
+1-GPU blend of the same tiles bit for bit.
 
-    torchrun --nproc-per-node P --master-addr 127.0.0.1 scripts/vae_blend_check.py
+    [AQB_OVERSUBSCRIBE=1] torchrun --nproc-per-node P --master-addr 127.0.0.1 tests/mp_vae_blend.py
 """
 import json
 import os
@@ -13,9 +14,10 @@ import torch
 import torch.distributed as dist
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-from paper_2505_10584_b200.parallel import Ulysses, init_from_env  # noqa: E402
+from paper_2505_10584_b200.parallel import Ulysses, init_from_env, oversubscribed  # noqa: E402
 from paper_2505_10584_b200.tiling import PeerTiles, blend_tiles, plan_vae_tiles  # noqa: E402
 
+OUT = sys.argv[sys.argv.index("--out") + 1] if "--out" in sys.argv else None
 init_from_env("nccl")
 sp = Ulysses(exchange="p2p")
 ok = True
@@ -41,11 +43,15 @@ for latent, tile, ov in (((9, 40, 64), (5, 16, 24), (1, 4, 8)), ((33, 90, 160), 
     same = torch.equal(out, ref)
     ok &= same
     if sp.rank == 0:
-        print(json.dumps({"P": sp.P, "latent": latent, "tiles": len(plan.tiles), "bitwise_vs_1gpu": same,
-                          "max_abs": float((out - ref).abs().max())}), flush=True)
+        rec = json.dumps({"P": sp.P, "latent": latent, "tiles": len(plan.tiles), "bitwise_vs_1gpu": same,
+                          "max_abs": float((out - ref).abs().max())})
+        print(rec, flush=True)
+        if OUT:
+            with open(OUT, "a") as fh:
+                fh.write(rec + "\n")
     dist.barrier()
     pt.close()
-flag = torch.tensor([1 if ok else 0], device="cuda")
+flag = torch.tensor([1 if ok else 0], device="cpu" if oversubscribed() else "cuda")
 dist.all_reduce(flag, op=dist.ReduceOp.MIN)
 dist.destroy_process_group()
 sys.exit(0 if int(flag) else 1)

@@ -47,3 +47,18 @@ def test_multirank_parity(parallel, P, tmp_path):
         assert len(x["schedule_per_rank"]) == P
         assert all(s == x["schedule_oracle"] for s in x["schedule_per_rank"])
         assert "c" in x["schedule_oracle"]  # cached steps on every rank, every policy
+
+
+@pytest.mark.parametrize("P", [2, 4])
+def test_multirank_vae_tile_blend(P, tmp_path):
+    """Multi-GPU VAE blend (PeerTiles): each rank's tiles read from its peer memory blend to the
+    same bits as the 1-GPU blend (the worker exits 1 otherwise)."""
+    out = tmp_path / "blend.jsonl"
+    env = dict(os.environ, AQB_OVERSUBSCRIBE="1", OMP_NUM_THREADS="2")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={P}",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(ROOT, "tests", "mp_vae_blend.py"),
+           "--out", str(out)]
+    r = subprocess.run(cmd, env=env, cwd=ROOT, capture_output=True, text=True, timeout=600)
+    lines = [json.loads(x) for x in out.read_text().splitlines()] if out.exists() else []
+    assert r.returncode == 0 and len(lines) == 2, (r.returncode, r.stdout[-2000:], r.stderr[-2000:])
+    assert all(x["bitwise_vs_1gpu"] for x in lines)

@@ -130,7 +130,7 @@ def test_window_average_kernel(n_prime, n, s, hw):
 @pytest.mark.gpu
 def test_peer_tiles_single_rank_blend_equals_local_blend():
     """PeerTiles (multi-GPU VAE blend) with a group of one: tiles written into the peer buffer
-    blend to the same bits as the plain blend of the same tiles (scripts/vae_blend_check.py: P=2)."""
+    blend to the same bits as the plain blend of the same tiles (multi-rank: tests/test_multirank_gpu.py::test_multirank_vae_tile_blend)."""
     import socket
 
     import torch.distributed as dist
