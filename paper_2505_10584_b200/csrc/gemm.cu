@@ -304,7 +304,15 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
     for (int hc = 0; hc < BN; hc += 128) {
       const int colh = col_base + hc;
       if (hc >= width || colh >= p.N) break;
+      // bias requested before the accumulator load (its latency overlaps it; -0 is the
+      // additive identity, so the sum has the same bits as adding after)
       float v[128];
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const float4 bb = p.bias != nullptr ? __ldg(reinterpret_cast<const float4*>(p.bias + colh) + i)
+                                            : make_float4(-0.f, -0.f, -0.f, -0.f);
+        v[4 * i] = bb.x, v[4 * i + 1] = bb.y, v[4 * i + 2] = bb.z, v[4 * i + 3] = bb.w;
+      }
       {
         uint32_t u[32];
 #pragma unroll
@@ -312,15 +320,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           tmem_ld32(tacc + hc + 32 * h + lane_off, u);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[32 * h + i] = __uint_as_float(u[i]);
-        }
-      }
-      if (p.bias != nullptr) {
-        const float4* b4 = reinterpret_cast<const float4*>(p.bias + colh);
-#pragma unroll
-        for (int i = 0; i < 32; ++i) {
-          const float4 bb = __ldg(b4 + i);
-          v[4 * i] += bb.x, v[4 * i + 1] += bb.y, v[4 * i + 2] += bb.z, v[4 * i + 3] += bb.w;
+          for (int i = 0; i < 32; ++i) v[32 * h + i] += __uint_as_float(u[i]);
         }
       }
       const int part = colh / p.part_width;
@@ -415,7 +415,24 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
         if (leader_thread) bulk_wait_read<NB - 1>();
         named_bar_sync(1, 128);
       }
+      // bias and gate are requested before the accumulator load so their L2 latency
+      // overlaps it (acc + bias == bias + acc: the same bits as adding after)
       float v[CW];
+#pragma unroll
+      for (int i = 0; i < CW / 4; ++i) {
+        const float4 bb = (p.bias != nullptr && col0 + 4 * i < p.N)
+                              ? __ldg(reinterpret_cast<const float4*>(p.bias + col0) + i)
+                              : make_float4(-0.f, -0.f, -0.f, -0.f);  // -0: the additive identity
+        v[4 * i] = bb.x, v[4 * i + 1] = bb.y, v[4 * i + 2] = bb.z, v[4 * i + 3] = bb.w;
+      }
+      constexpr bool kGate = EPI == AQB_EPI_GATE_RES || EPI == kEpiGateAdd || EPI == kEpiGateAddScatter;
+      float4 gr[kGate ? 8 : 1];
+      if constexpr (kGate) {
+        const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+          gr[i] = (p.gate && col0 + 4 * i < p.N) ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+      }
       {
         uint32_t u[32];
 #pragma unroll
@@ -423,17 +440,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           tmem_ld32(tacc + c + 32 * h + lane_off, u);
           tmem_wait_ld();
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[32 * h + i] = __uint_as_float(u[i]);
-        }
-      }
-      if (p.bias != nullptr) {
-        const float4* b4 = reinterpret_cast<const float4*>(p.bias + col0);
-#pragma unroll
-        for (int i = 0; i < CW / 4; ++i) {
-          if (col0 + 4 * i < p.N) {
-            const float4 bb = __ldg(b4 + i);
-            v[4 * i] += bb.x, v[4 * i + 1] += bb.y, v[4 * i + 2] += bb.z, v[4 * i + 3] += bb.w;
-          }
+          for (int i = 0; i < 32; ++i) v[32 * h + i] += __uint_as_float(u[i]);
         }
       }
       const uint32_t rowaddr = smem_u32(buf) + r * 128;
@@ -446,7 +453,6 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
         }
         mbar_wait(es.bar + b, (es.phase_bits >> b) & 1);
         es.phase_bits ^= 1u << b;
-        const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
         const uint32_t arow = smem_u32(abuf) + r * 64, asw = (r >> 1) & 3;
 #pragma unroll
         for (int i = 0; i < 8; i += 2) {
@@ -455,8 +461,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           for (int h = 0; h < 2; ++h) {
             const uint32_t a = rowaddr + (((i + h) ^ sw) << 4);
             const uint4 xr = lds128(a);
-            const float4 g = (p.gate && col0 + 4 * (i + h) < p.N) ? __ldg(g4 + i + h)
-                                                                    : make_float4(1.f, 1.f, 1.f, 1.f);
+            const float4 g = gr[i + h];
             nx[4 * h + 0] = __uint_as_float(xr.x) + g.x * v[4 * (i + h)];
             nx[4 * h + 1] = __uint_as_float(xr.y) + g.y * v[4 * (i + h) + 1];
             nx[4 * h + 2] = __uint_as_float(xr.z) + g.z * v[4 * (i + h) + 2];
@@ -474,12 +479,11 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(v[4 * i]), __float_as_uint(v[4 * i + 1]),
                        __float_as_uint(v[4 * i + 2]), __float_as_uint(v[4 * i + 3]));
       } else if constexpr (EPI == kEpiGateAddScatter) {
-        const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
         const int64_t first = int64_t(row0), last = min(int64_t(row0) + BM, int64_t(p.M)) - 1;
         if (first / p.red_rpr == last / p.red_rpr) {  // CTA block inside one rank: stage for TMA
 #pragma unroll
           for (int i = 0; i < 8; ++i) {
-            const float4 g = (p.gate && col0 + 4 * i < p.N) ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+            const float4 g = gr[i];
             st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(g.x * v[4 * i]),
                          __float_as_uint(g.y * v[4 * i + 1]), __float_as_uint(g.z * v[4 * i + 2]),
                          __float_as_uint(g.w * v[4 * i + 3]));
@@ -492,7 +496,7 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
 #pragma unroll
             for (int i = 0; i < 8; ++i) {
               if (col0 + 4 * i < p.N) {
-                const float4 g = p.gate ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+                const float4 g = gr[i];
                 red_add_v4_sys(dst + 4 * i, g.x * v[4 * i], g.y * v[4 * i + 1], g.z * v[4 * i + 2],
                                g.w * v[4 * i + 3]);
               }
@@ -502,10 +506,9 @@ __device__ __forceinline__ void epilogue_tile(const Params& p, const CUtensorMap
           continue;  // uniform: no staged tile, no TMA op for this chunk
         }
       } else if constexpr (EPI == kEpiGateAdd) {
-        const float4* g4 = reinterpret_cast<const float4*>(p.gate + col0);
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          const float4 g = (p.gate && col0 + 4 * i < p.N) ? __ldg(g4 + i) : make_float4(1.f, 1.f, 1.f, 1.f);
+          const float4 g = gr[i];
           st_shared_v4(rowaddr + ((i ^ sw) << 4), __float_as_uint(g.x * v[4 * i]), __float_as_uint(g.y * v[4 * i + 1]),
                        __float_as_uint(g.z * v[4 * i + 2]), __float_as_uint(g.w * v[4 * i + 3]));
         }
