@@ -193,6 +193,10 @@ int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t h
  * writes clock64 stamps of its pipeline events; NULL (default) disables.  Not thread-safe
  * against concurrent launches; a measurement aid, off the product path. */
 int aqb_attention_trace(void* buffer);
+/* Profiling hook: device buffer (>= 128 * CTAs uint64) into which the GEMM kernels write
+ * clock64 stamps (entry, after the PDL wait, each k-block the MMA warp consumes, each tile's
+ * epilogue start / end); NULL (default) disables.  A measurement aid, off the product path. */
+int aqb_gemm_trace(void* buffer);
 /* The automatic split-KV plan: out[5] = {whole tiles, splits, KV blocks of split 0, KV blocks of
  * each later split, split-major launch order (0/1)}. */
 int aqb_attention_plan(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t head_dim, int32_t* out);

@@ -25,6 +25,7 @@ SIGNATURES = {
     "aqb_sm_count": (c_int, []),
     "aqb_set_pdl": (c_int, [c_int]),
     "aqb_attention_trace": (c_int, [P]),
+    "aqb_gemm_trace": (c_int, [P]),
     "aqb_attention_plan": (c_int, [c_int64, c_int64, c_int32, c_int32, P]),
     "aqb_norm_modulate": (c_int, [P, c_int64, P, P, P, c_int64, c_int64, c_int32, c_float, c_int32, P, P, P, c_int32, P]),
     "aqb_gate_bcast": (c_int, [P, c_int64, P, P, c_int32, c_int64, c_int64, c_int64, P, c_int32, P]),

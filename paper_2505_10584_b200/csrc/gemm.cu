@@ -26,6 +26,7 @@
 // and one thread TMA-stores the chunk.  All global traffic is TMA (coalesced);
 // the two smem buffers alternate so a chunk's store overlaps the next chunk.
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
@@ -86,7 +87,24 @@ struct Params {
   // gate-add scatter (kEpiGateAddScatter): rank r's residual, rows_per_rank rows of stride ldo
   float* red_dst[8];
   int64_t red_rpr;
+  // profiling hook (aqb_gemm_trace): per CTA 128 clock64 stamps (see gstamp); null: off
+  unsigned long long* trace;
 };
+
+// Trace slots per CTA: 0 entry, 1 entry globaltimer, 2 setup done, 3 after the PDL wait,
+// 8 + i: MMA warp passes the full barrier of its i-th k-block (i < 96; pair kernel: leader),
+// 104 + 2j / 105 + 2j: epilogue warp 4 sees tile j's accumulator / finishes it (j < 8),
+// 120: epilogue stores drained, 121: exit globaltimer.
+__device__ __forceinline__ void gstamp(const Params& p, int slot, bool global_timer = false) {
+  if (p.trace != nullptr) {
+    unsigned long long t;
+    if (global_timer)
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    else
+      t = clock64();
+    p.trace[int64_t(blockIdx.x) * 128 + slot] = t;
+  }
+}
 
 // Per-destination-rank output maps of the Ulysses scatter (QK-norm epilogue):
 // map g addresses this rank's row block inside rank g's attention-input buffer.
@@ -571,6 +589,8 @@ __global__ void __launch_bounds__(kThreads, 1)
   const uint32_t warp = warp_idx(), lane = lane_idx();
 
   if (warp == 0 && lane == 0) {
+    gstamp(p, 0);
+    gstamp(p, 1, true);
     tma_prefetch_desc(&tma_a);
     tma_prefetch_desc(&tma_b);
     tma_prefetch_desc(&tma_o);
@@ -592,9 +612,11 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nk = (p.K + BK - 1) / BK;
+  if (threadIdx.x == 0) gstamp(p, 2);
   // the prologue above overlaps the previous kernel's tail (PDL); inputs only after this
   pdl_wait();
   pdl_trigger();
+  if (threadIdx.x == 0) gstamp(p, 3);
   const bool run = gate_open(p.run_flag, p.run_if);
 
   if (!run) {
@@ -621,6 +643,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     uint32_t phase = 0;
     int acc = 0;
     uint32_t acc_phase = 0;
+    int kseen = 0;
     for (int t = blockIdx.x; t < p.num_units; t += gridDim.x) {
       mbar_wait(tempty + acc, acc_phase ^ 1);
       tc_fence_after();
@@ -628,6 +651,8 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kb = 0; kb < nk; ++kb) {
         mbar_wait(full + stage, phase);
         tc_fence_after();
+        if (lane == 0 && kseen < 96) gstamp(p, 8 + kseen);
+        ++kseen;
         const uint32_t a0 = smem_u32(sa + stage * BM * BK);
         const uint32_t b0 = smem_u32(sb + stage * BN * BK);
 #pragma unroll
@@ -648,20 +673,27 @@ __global__ void __launch_bounds__(kThreads, 1)
     EpiState es{ebuf, ebar, 0, int(blockIdx.x), int(gridDim.x), BM, 0, 0, 0, 0, nullptr, nullptr, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int t = blockIdx.x; t < p.num_units; t += gridDim.x) {
+    int j = 0;
+    for (int t = blockIdx.x; t < p.num_units; t += gridDim.x, ++j) {
       int mb, nb;
       tile_coords(p, t, mb, nb);
       epilogue_prologue<EPI, BN, NB>(p, &tma_o, &pm, es, mb * BM, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
+      if (q == 0 && lane == 0 && j < 8) gstamp(p, 104 + 2 * j);
       epilogue_tile<EPI, BN, NB>(p, &tma_o, &pm, es, tmem + acc * BN, mb * BM, nb * BN, BN, q, lane);
+      if (q == 0 && lane == 0 && j < 8) gstamp(p, 105 + 2 * j);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(tempty + acc);
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (q == 0 && lane == 0) bulk_wait<0>();
+    if (q == 0 && lane == 0) {
+      bulk_wait<0>();
+      gstamp(p, 120);
+      gstamp(p, 121, true);
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -700,6 +732,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
 
   if (warp == 0 && lane == 0) {
+    gstamp(p, 0);
+    gstamp(p, 1, true);
     tma_prefetch_desc(&tma_a);
     tma_prefetch_desc(&tma_b);
     tma_prefetch_desc(&tma_o);
@@ -722,8 +756,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   const int nk = (p.K + BK - 1) / BK;
+  if (threadIdx.x == 0) gstamp(p, 2);
   pdl_wait();  // prologue overlapped the previous kernel (PDL); inputs only after this
   pdl_trigger();
+  if (threadIdx.x == 0) gstamp(p, 3);
   const bool run = gate_open(p.run_flag, p.run_if);
 
   if (!run) {
@@ -762,6 +798,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
+      int kseen = 0;
       for (int u = cluster; u < p.num_units; u += nclusters) {
         const uint32_t idesc = u < p.n_full ? kIdesc : kIdescHalf;
         mbar_wait(tempty + acc, acc_phase ^ 1);
@@ -770,6 +807,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
         for (int kb = 0; kb < nk; ++kb) {
           mbar_wait(full + stage, phase);
           tc_fence_after();
+          if (lane == 0 && kseen < 96) gstamp(p, 8 + kseen);
+          ++kseen;
           const uint32_t a0 = smem_u32(sa + stage * kABytes);
           const uint32_t b0 = smem_u32(sb + stage * kBBytes);
 #pragma unroll
@@ -791,14 +830,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
                 rope_bytes<EPI, true>() ? rope_buf : nullptr, rbar, 0};
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int u = cluster; u < p.num_units; u += nclusters) {
+    int j = 0;
+    for (int u = cluster; u < p.num_units; u += nclusters, ++j) {
       int mb, col0, width;
       unit_coords<BN>(p, u, mb, col0, width);
       epilogue_prologue<EPI, BN, NB>(p, &tma_o, &pm, es, mb * (2 * BM) + int(rank) * BM, q == 0 && lane == 0);
       mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
+      if (q == 0 && lane == 0 && j < 8) gstamp(p, 104 + 2 * j);
       epilogue_tile<EPI, BN, NB>(p, &tma_o, &pm, es, tmem + acc * BN, mb * (2 * BM) + rank * BM, col0, width, q,
                                  lane);
+      if (q == 0 && lane == 0 && j < 8) gstamp(p, 105 + 2 * j);
       tc_fence_before();
       __syncwarp();
       if (lane == 0) {
@@ -810,7 +852,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
       acc ^= 1;
       if (acc == 0) acc_phase ^= 1;
     }
-    if (q == 0 && lane == 0) bulk_wait<0>();
+    if (q == 0 && lane == 0) {
+      bulk_wait<0>();
+      gstamp(p, 120);
+      gstamp(p, 121, true);
+    }
   }
   tc_fence_before();
   cluster_sync();
@@ -875,6 +921,9 @@ int dispatch_epi(int epi, const CUtensorMap& ta, const CUtensorMap& tb, const CU
 // bytes each SM loads.  AQB_GEMM_VARIANT=1cta256|1cta128|2cta256|2cta128
 // forces one (benchmarking).
 enum Variant { V1_256 = 0, V1_128, V2_256, V2_128 };
+
+// aqb_gemm_trace: device buffer [grid][128] of pipeline stamps for the next launches (null: off)
+static std::atomic<unsigned long long*> g_gemm_trace{nullptr};
 
 // AQB_GEMM_GATE_ADD=0: gate*residual always through the residual-reading epilogue (benchmarking)
 static bool gate_add_enabled() {
@@ -998,6 +1047,7 @@ static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m
     p.n_full = p.num_tiles - tail;
   }
   p.num_units = p.n_full + 2 * (p.num_tiles - p.n_full);
+  p.trace = g_gemm_trace.load();
   switch (variant) {
     case V1_256: return dispatch_epi<256, 4, false>(epilogue, ta, tb, to, pm, p, s);
     case V1_128: return dispatch_epi<128, 6, false>(epilogue, ta, tb, to, pm, p, s);
@@ -1192,4 +1242,9 @@ extern "C" int aqb_gemm_gate_add_scatter(const void* a, int64_t lda, const void*
   }
   return run(a, lda, w, ldw, m, n, k, kEpiGateAddScatter, p, pm.m[0], pick_variant(m, n, k, true),
              reinterpret_cast<cudaStream_t>(stream), &pm);
+}
+
+extern "C" int aqb_gemm_trace(void* buffer) {
+  aqb::gemm::g_gemm_trace.store(reinterpret_cast<unsigned long long*>(buffer));
+  return AQB_OK;
 }
