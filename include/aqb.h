@@ -195,7 +195,9 @@ int aqb_attention_splits(int64_t seq_q, int64_t seq_kv, int32_t heads, int32_t h
 int aqb_attention_trace(void* buffer);
 /* Profiling hook: device buffer (>= 128 * CTAs uint64) into which the GEMM kernels write
  * clock64 stamps (entry, after the PDL wait, each k-block the MMA warp consumes, each tile's
- * epilogue start / end); NULL (default) disables.  A measurement aid, off the product path. */
+ * epilogue start / end); NULL (default) disables.  A measurement aid, off the product path:
+ * compiled in only by a build with AQB_BUILD_DEFINES=-DAQB_GEMM_TRACE, otherwise a non-NULL
+ * buffer returns AQB_EINVAL. */
 int aqb_gemm_trace(void* buffer);
 /* The automatic split-KV plan: out[5] = {whole tiles, splits, KV blocks of split 0, KV blocks of
  * each later split, split-major launch order (0/1)}. */

@@ -35,9 +35,19 @@ def nvcc() -> str:
     raise RuntimeError("nvcc not found; cannot build libaqb.so")
 
 
+def _defines_file() -> str:
+    return os.path.join(HERE, "_obj", "defines.txt")
+
+
 def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
+    try:  # a library built with other AQB_BUILD_DEFINES (e.g. a trace build) is stale
+        with open(_defines_file()) as fh:
+            if fh.read() != os.environ.get("AQB_BUILD_DEFINES", ""):
+                return True
+    except OSError:
+        pass
     t = os.path.getmtime(LIB)
     deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS] + [os.path.join(INCLUDE, "aqb.h")]
     return any(os.path.getmtime(d) > t for d in deps)
@@ -61,10 +71,11 @@ def build(force: bool = False, verbose: bool = False) -> str:
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f not in ("-shared", "-cudart", "static")]
     define = f'-DAQB_HEADER_HASH="{header_hash()}"'
+    extra = os.environ.get("AQB_BUILD_DEFINES", "").split()  # e.g. -DAQB_GEMM_TRACE (measurement builds)
 
     def compile_one(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [nvcc(), *compile_flags, define, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [nvcc(), *compile_flags, define, *extra, "-I", INCLUDE, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         res = subprocess.run(cmd, capture_output=True, text=True)
@@ -80,6 +91,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if res.returncode != 0:
         raise RuntimeError(f"nvcc link failed ({res.returncode}):\n{res.stderr[-8000:]}")
     os.replace(tmp, LIB)
+    with open(_defines_file(), "w") as fh:
+        fh.write(os.environ.get("AQB_BUILD_DEFINES", ""))
     return LIB
 
 

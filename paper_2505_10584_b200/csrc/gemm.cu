@@ -95,7 +95,10 @@ struct Params {
 // 8 + i: MMA warp passes the full barrier of its i-th k-block (i < 96; pair kernel: leader),
 // 104 + 2j / 105 + 2j: epilogue warp 4 sees tile j's accumulator / finishes it (j < 8),
 // 120: epilogue stores drained, 121: exit globaltimer.
+// Compiled in only with -DAQB_GEMM_TRACE (AQB_BUILD_DEFINES=-DAQB_GEMM_TRACE at build time): the
+// per-k-block check cost 0.3-1% on the small shards when always present.
 __device__ __forceinline__ void gstamp(const Params& p, int slot, bool global_timer = false) {
+#ifdef AQB_GEMM_TRACE
   if (p.trace != nullptr) {
     unsigned long long t;
     if (global_timer)
@@ -104,6 +107,9 @@ __device__ __forceinline__ void gstamp(const Params& p, int slot, bool global_ti
       t = clock64();
     p.trace[int64_t(blockIdx.x) * 128 + slot] = t;
   }
+#else
+  (void)p, (void)slot, (void)global_timer;
+#endif
 }
 
 // Per-destination-rank output maps of the Ulysses scatter (QK-norm epilogue):
@@ -1245,6 +1251,11 @@ extern "C" int aqb_gemm_gate_add_scatter(const void* a, int64_t lda, const void*
 }
 
 extern "C" int aqb_gemm_trace(void* buffer) {
+#ifdef AQB_GEMM_TRACE
   aqb::gemm::g_gemm_trace.store(reinterpret_cast<unsigned long long*>(buffer));
   return AQB_OK;
+#else
+  if (buffer == nullptr) return AQB_OK;
+  return aqb::set_error(AQB_EINVAL, "aqb_gemm_trace: library built without -DAQB_GEMM_TRACE");
+#endif
 }

@@ -4,7 +4,10 @@ back-to-back launches in a CUDA graph (the `scripts/gemm_bench.py` harness), sum
 cycles from the PDL wait: first k-block consumed, median k-block interval, tile epilogue
 start/end, drain; plus the entry/exit spread of the CTAs (globaltimer, ns).
 
+    AQB_BUILD_DEFINES=-DAQB_GEMM_TRACE python -c "from paper_2505_10584_b200 import build; build.build(force=True)"
     python scripts/gemm_trace.py proj 1950 2048 2048 [more cases as name m n k ...]
+
+(the stamps are compiled in only by that build; rebuild without the define afterwards)
 """
 
 import json
