@@ -754,12 +754,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(kThreads, 1)
     for (int b = 0; b < NB; ++b) mbar_init(ebar + b, 1);
     mbar_init(ebar + NB, 1);  // rope tables (QK-norm epilogue)
     fence_barrier_init();
+    gstamp(p, 4);
   }
-  cluster_sync();
-  if (warp == 2) tmem_alloc_pair(tmem_slot, kTmemCols);
+  // one cluster barrier publishes both the initialised mbarriers (before any remote arrive or
+  // pair TMA signals them) and the pair TMEM allocation (written to this CTA's own smem);
+  // a second barrier between the two cost 700-1,200 cycles of prologue per launch
+  if (warp == 2) {
+    tmem_alloc_pair(tmem_slot, kTmemCols);
+    if (lane == 0) gstamp(p, 6);
+  }
   tc_fence_before();
   cluster_sync();
   tc_fence_after();
+  if (threadIdx.x == 0) gstamp(p, 7);
   const uint32_t tmem = *tmem_slot;
   const int nk = (p.K + BK - 1) / BK;
   if (threadIdx.x == 0) gstamp(p, 2);

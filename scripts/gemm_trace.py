@@ -42,6 +42,7 @@ def trace_case(name, m, n, k):
         d = [b - a for a, b in zip(ks, ks[1:])]
         ep = [(s[104 + 2 * j] - w, s[105 + 2 * j] - w) for j in range(8) if s[104 + 2 * j] != 0]
         rows.append({"cta": c, "setup": s[2] - s[0], "pdl_wait": w - s[2],
+                     "pro": [s[i] - s[0] if s[i] else None for i in (4, 6, 7)],  # init, alloc, cluster sync
                      "first_k": (ks[0] - w) if ks else None, "last_k": (ks[-1] - w) if ks else None,
                      "k_blocks": len(ks), "k_med": statistics.median(d) if d else None,
                      "k_max": max(d) if d else None, "epi": ep, "drained": s[120] - w if s[120] else None,
