@@ -26,11 +26,11 @@ import gemm_bench  # noqa: E402
 
 def trace_case(name, m, n, k):
     tr = torch.zeros(4096 * 128, dtype=torch.int64, device="cuda")
-    _native.query("aqb_gemm_trace", tr.data_ptr())
+    _native.call("aqb_gemm_trace", tr.data_ptr())  # raises unless a trace build
     try:
         r = gemm_bench.case(name, m, n, k)
     finally:
-        _native.query("aqb_gemm_trace", None)
+        _native.call("aqb_gemm_trace", None)
     torch.cuda.synchronize()
     t = tr.view(-1, 128).cpu()
     ctas = [i for i in range(t.shape[0]) if int(t[i, 0]) != 0]

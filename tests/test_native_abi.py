@@ -92,6 +92,17 @@ def test_peer_barrier_validates_before_launch(lib_path):
     assert lib.aqb_peer_barrier(arr, 0, 9, 64, None, 0, None, None, None, 1, None) == -1  # > 8 ranks
 
 
+def test_gemm_trace_is_a_measurement_build_only(lib_path):
+    """aqb_gemm_trace: NULL (off) always succeeds; a buffer is refused unless the library was built
+    with -DAQB_GEMM_TRACE (the shipped build has no per-k-block stamp checks)."""
+    if "AQB_GEMM_TRACE" in os.environ.get("AQB_BUILD_DEFINES", ""):
+        pytest.skip("trace build")
+    lib = _native.load()
+    assert lib.aqb_gemm_trace(None) == 0
+    assert lib.aqb_gemm_trace(ctypes.c_void_p(4096)) == -1
+    assert b"AQB_GEMM_TRACE" in lib.aqb_last_error()
+
+
 def test_kernel_kind_mapping_of_trace_symbols():
     """bench's CUPTI table groups libaqb kernels by symbol; foreign kernels (torch) are ignored."""
     from paper_2505_10584_b200.ops import kernel_kind
