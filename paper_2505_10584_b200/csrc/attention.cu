@@ -681,6 +681,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t q_addr = __shfl_sync(0xffffffffu, smem_u32(sQ), 0);
     const uint32_t k_addr = __shfl_sync(0xffffffffu, smem_u32(sK), 0);
     const uint32_t v_addr = __shfl_sync(0xffffffffu, smem_u32(sV), 0);
+    // keys past seq_kv (short text, e.g. 77 tokens): no QK^T for an all-padding 128-key block,
+    // no PV steps past the last 16 keys that hold a valid one (their P is masked to 0)
+    const int nkb = p.seq_kv > BKV ? 2 : 1;
+    const int nkk = (p.seq_kv + 15) / 16;
     auto qk = [&](int i) {
       const int b = i & 1, sl = i & 1;
       if (i >= 2) {  // slot reused: the epilogue of tile i-2 has read O out of it
@@ -693,6 +697,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       const uint32_t a0 = q_addr + b * C::kQBytes;
 #pragma unroll
       for (int kb = 0; kb < 2; ++kb) {
+        if (kb >= nkb) break;
         const uint32_t b0 = k_addr + kb * C::kKVBlock;
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) {
@@ -711,6 +716,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       if (lane == 0 && i < 8) short_stamp(p, 8 + i);
 #pragma unroll
       for (int kk = 0; kk < 16; ++kk) {  // 16 keys per MMA (8 packed TMEM columns of P)
+        if (kk >= nkk) break;
         const uint64_t db = smem_desc(v_addr + (kk >> 3) * C::kKVBlock + (kk & 7) * 16 * 128, BKV * 128, 1024);
         if (elect_one()) umma_bf16_ts(tm + sl * 256 + 128, tm + sl * 256 + kk * 8, db, kIdescO, kk > 0);
       }
@@ -737,6 +743,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const uint32_t s_tmem = tmem + lane_base + wg * 256;
     const float c = p.scale_log2;
     const uint64_t c2 = f2pack(c, c);
+    const int nh = min(4, (p.seq_kv + 63) / 64);  // 64-key chunks holding a valid key (the PV reads no more)
     for (int i = wg; i < ntile; i += 2) {
       const uint32_t ph = (i >> 1) & 1;
       mbar_wait(s_full + wg, ph);
@@ -747,7 +754,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       // pass 1: row max over the valid keys, 64 columns at a time
       float mx = -INFINITY;
 #pragma unroll 1
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < nh; ++h) {
         tmem_ld64(s_tmem + h * 64, sr);
         tmem_wait_ld();
         const int valid = p.seq_kv - h * 64;
@@ -775,7 +782,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
       for (int q = 0; q < 4; ++q) acc2[q] = f2pack(0.f, 0.f);
 #pragma unroll 1
-      for (int h = 0; h < 4; ++h) {
+      for (int h = 0; h < nh; ++h) {
         tmem_ld64(s_tmem + h * 64, sr);
         tmem_wait_ld();
         const int valid = p.seq_kv - h * 64;
