@@ -1048,7 +1048,20 @@ static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m
   p.num_m = int((m + tile_m - 1) / tile_m);
   p.num_n = int((n + bn - 1) / bn);
   p.num_tiles = p.num_m * p.num_n;
-  p.group_m = 16;
+  {
+    // Raster: tiles walk M first inside groups of group_m M blocks.  Narrow outputs (<= 16
+    // column tiles: the out-projections and FFN2) take groups of 4, so a wave covers every
+    // column tile of a few row blocks and each A row block is read while it is L2-resident —
+    // measured in a CUDA graph (`profiles/r02_gemm_group_m.jsonl`): FFN2 7800x2048x8192
+    // 190.2 -> 184.1 us, out-projection 3900x2048x2048 39.1 -> 35.5, MM-DiT 25696x3072x3072
+    // 382 -> 370; wide outputs (QKV, FFN1) keep 16.  AQB_GEMM_GROUP_M forces (benchmarking).
+    static int gm = -1;
+    if (gm < 0) {
+      const char* e = getenv("AQB_GEMM_GROUP_M");
+      gm = e ? std::max(1, atoi(e)) : 0;
+    }
+    p.group_m = gm > 0 ? gm : (p.num_n <= 16 ? 4 : 16);
+  }
   p.n_full = p.num_tiles;
   const int tail = half_tail_tiles(p.num_tiles, pair, bn);
   if (tail > 0) {  // the last `tail` tiles run as two half-width units each
