@@ -1049,18 +1049,22 @@ static int run(const void* a, int64_t lda, const void* w, int64_t ldw, int64_t m
   p.num_n = int((n + bn - 1) / bn);
   p.num_tiles = p.num_m * p.num_n;
   {
-    // Raster: tiles walk M first inside groups of group_m M blocks.  Narrow outputs (<= 16
-    // column tiles: the out-projections and FFN2) take groups of 4, so a wave covers every
-    // column tile of a few row blocks and each A row block is read while it is L2-resident —
-    // measured in a CUDA graph (`profiles/r02_gemm_group_m.jsonl`): FFN2 7800x2048x8192
-    // 190.2 -> 184.1 us, out-projection 3900x2048x2048 39.1 -> 35.5, MM-DiT 25696x3072x3072
-    // 382 -> 370; wide outputs (QKV, FFN1) keep 16.  AQB_GEMM_GROUP_M forces (benchmarking).
+    // Raster: tiles walk M first inside groups of group_m M blocks.  With small groups a wave
+    // covers every column tile of a few row blocks (each A row block is consumed while
+    // L2-resident, all of W streams per wave); with groups of 16 it covers a few column tiles
+    // of 16 row blocks (a W column slab stays resident instead).  Measured in a CUDA graph
+    // (`profiles/r02_gemm_group_m.jsonl`, interleaved repeats): groups of 2 when W fits well in
+    // L2 (<= 40 MB: every config-2 weight; QKV 7800x6144x2048 135.8 -> 132.4 us, FFN2
+    // 7800x2048x8192 190.2 -> 184.1, out-projection 3900x2048x2048 39.1 -> 35.5), else 4 for
+    // narrow outputs and 16 for wide ones (MM-DiT QKV / FFN1 with 57-75 MB of W: 16 is 5-10%
+    // faster than 2-4).  AQB_GEMM_GROUP_M forces (benchmarking).
     static int gm = -1;
     if (gm < 0) {
       const char* e = getenv("AQB_GEMM_GROUP_M");
       gm = e ? std::max(1, atoi(e)) : 0;
     }
-    p.group_m = gm > 0 ? gm : (p.num_n <= 16 ? 4 : 16);
+    const bool w_fits = n * k * 2 <= (int64_t(40) << 20);
+    p.group_m = gm > 0 ? gm : w_fits ? 2 : (p.num_n <= 16 ? 4 : 16);
   }
   p.n_full = p.num_tiles;
   const int tail = half_tail_tiles(p.num_tiles, pair, bn);
