@@ -6,8 +6,8 @@ MM-DiT 720p shard).  Two timings per shape:
 * ``graph``: 24 launches captured in one CUDA graph over 8 rotating x/y buffer sets
   (> L2 in total), so consecutive launches overlap their prologues like in the model.
 
-Bytes per launch = rows·H·(4 + 2) (f32 in, bf16 out).  ``AQB_NORM_TMA=0`` selects the
-previous CTA-per-row kernel (the env is read once per process: run twice).
+Bytes per launch = rows·H·(4 + 2) (f32 in, bf16 out).  ``--ncu rows H``: two launches of one
+shape and nothing else (for ``ncu -k regex:norm_mod_row -s 1 -c 1``).
 """
 
 import json
@@ -22,7 +22,19 @@ from paper_2505_10584_b200 import ops  # noqa: E402
 dev = "cuda"
 
 
+def once(rows, H):
+    x = torch.randn(rows, H, device=dev)
+    y = torch.empty(rows, H, device=dev, dtype=torch.bfloat16)
+    sh, sc = torch.randn(H, device=dev), torch.randn(H, device=dev)
+    for _ in range(2):
+        ops.norm_modulate(x, sh, sc, y)
+    torch.cuda.synchronize()
+
+
 def main():
+    if len(sys.argv) > 1 and sys.argv[1] == "--ncu":
+        once(int(sys.argv[2]), int(sys.argv[3]))
+        return
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     out = []
     for rows, H in ((7800, 2048), (3900, 2048), (1950, 2048), (975, 2048), (15106, 3072), (25696, 3072),
@@ -62,7 +74,7 @@ def main():
             gt.append(e0.elapsed_time(e1) / 24)
         graph = sorted(gt)[len(gt) // 2]
         byt = rows * H * 6
-        rec = {"rows": rows, "hidden": H, "tma": os.environ.get("AQB_NORM_TMA", "1") != "0",
+        rec = {"rows": rows, "hidden": H,
                "single_us": single * 1e3, "single_gbs": byt / single / 1e6,
                "graph_us": graph * 1e3, "graph_gbs": byt / graph / 1e6}
         out.append(rec)
