@@ -40,8 +40,11 @@ PEAK_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustaine
 
 
 def traffic(kind):
-    """ncu-measured DRAM bytes per launch of the dominant kernel class (profiles/r01_traffic.json)."""
-    p = os.path.join(ROOT, "profiles", "r01_traffic.json")
+    """ncu-measured DRAM bytes per launch of the dominant kernel class (profiles/r02_traffic.json,
+    the final round-2 captures; r01_traffic.json if absent)."""
+    p = os.path.join(ROOT, "profiles", "r02_traffic.json")
+    if not os.path.exists(p):
+        p = os.path.join(ROOT, "profiles", "r01_traffic.json")
     if not os.path.exists(p):
         return None, None
     with open(p) as fh:
